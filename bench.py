@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Throughput bench of the SnapMLA FP8 MLA decode hot path on B200.
+
+One step = the whole hot path for one decode token per request on one MLA
+layer: mla_kv_append_quant (a1) -> mla_decode_fp8 (Q-quant prologue, a2-a9)
+-> mla_combine (a10), inputs resident in HBM.  Workload (N = 1, per rank):
+BASELINE.json configs[1], DeepSeek-R1 MLA layer: 128 q-heads, batch 64,
+context 32K, FP8 latent + BF16 RoPE, page 64.  N > 1: each rank runs the same
+per-rank workload on its own requests (batch partition, no data-path
+collective) -> "scaling": "weak"; value = tokens of all ranks / max-rank time.
+`--mode tp` instead partitions heads (BASELINE.json configs[2] shape) and
+all-gathers the output over NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP8 MLA decode tokens/s per B200 and % of HBM roofline, at 1/2/4/8 GPUs"
+BYTES_PER_TOKEN = 512 + 128 + 4      # FP8 latent + BF16 RoPE + fp32 scale
+WORKLOADS = {
+    "dsr1": dict(name="DeepSeek-R1 MLA layer decode: 128 q-heads, batch 64, context 32K, FP8 latent + BF16 RoPE",
+                 batch=64, heads=128, context=32768),
+    "dsr1_tp8": dict(name="DeepSeek-R1 TP8 shape: 16 q-heads/rank, batch 256, context 64K",
+                     batch=256, heads=16, context=65536),
+    "longcat": dict(name="LongCat-Flash-Thinking-shaped MLA decode, 64 q-heads, batch 128, context 128K",
+                    batch=128, heads=64, context=131072),
+    "tiny": dict(name="tiny MLA decode: batch 1, 16 q-heads, context 256", batch=1, heads=16, context=256),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="dsr1", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None, help="override per-rank batch")
+    ap.add_argument("--context", type=int, default=None)
+    ap.add_argument("--heads", type=int, default=None)
+    ap.add_argument("--mode", default="dp", choices=["dp", "tp"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(args):
+    w = dict(WORKLOADS[args.workload])
+    for k in ("batch", "context", "heads"):
+        v = getattr(args, k)
+        if v is not None:
+            w[k] = v
+    return w
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_key):
+    """dram bytes per decode launch from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e = d.get(workload_key)
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+# ------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_10718_b200 import ops, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workload(args)
+    B, H, L = w["batch"], w["heads"], w["context"]
+    heads_local = H // world if args.mode == "tp" else H
+    scale = synth.DEFAULT_SOFTMAX_SCALE
+
+    gen = torch.Generator(device=dev)
+    # TP replicas hold identical KV; DP ranks hold their own requests
+    gen.manual_seed(1234 + (0 if args.mode == "tp" else rank))
+    pages_per_req = (L + 63) // 64
+    num_pages = B * pages_per_req
+    cache = ops.PagedMLACache(num_pages, dev)
+    perm = torch.randperm(num_pages, generator=gen, device=dev).to(torch.int32)
+    block_table = perm.view(B, pages_per_req).contiguous()
+    # fill the cache with the product append kernel: every token is a one-token
+    # "request" (its page, its in-page row)
+    tok_chunk = 1 << 18
+    n_tok = B * L
+    for s in range(0, n_tok, tok_chunk):
+        idx = torch.arange(s, min(s + tok_chunk, n_tok), device=dev)
+        req, pos = idx // L, idx % L
+        bt_v = block_table[req, pos // 64].view(-1, 1).contiguous()
+        sl_v = (pos % 64 + 1).to(torch.int32)
+        c, r = synth.torch_latent(idx.numel(), gen, dev)
+        cache.append(c, r, bt_v, sl_v)
+    q_all = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
+    head0 = rank * heads_local if args.mode == "tp" else 0
+    q = q_all[:, head0:head0 + heads_local].contiguous()
+    new_c, new_r = synth.torch_latent(B, gen, dev)
+    seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
+    ws = torch.empty(ops.mla_decode_workspace_bytes(B, heads_local), dtype=torch.uint8, device=dev)
+    out = torch.empty(B, heads_local, 512, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(B, heads_local, dtype=torch.float32, device=dev)
+    gathered = torch.empty(world, B, heads_local, 512, dtype=torch.bfloat16, device=dev) if args.mode == "tp" else None
+    del q_all
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev_d0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_d1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step(i=None):
+        # a1: the new token of every request lands at position L-1 (same slot each step)
+        cache.append(new_c, new_r, block_table, seq_lens)
+        if i is not None:
+            ev_d0[i].record(stream)
+        ops.mla_decode_fp8(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        if i is not None:
+            ev_d1[i].record(stream)
+        ops.mla_combine(ws, B, heads_local, out, lse)
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    t_settle = time.time()
+    while time.time() - t_settle < 1.0:        # keep the GPU loaded so clocks are sampled under load
+        for _ in range(10):
+            step()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    dec_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_d0, ev_d1)]))
+    if world > 1:
+        t = torch.tensor([ms, dec_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, dec_ms = float(t[0]), float(t[1])
+    ms_step = ms / args.steps
+
+    # ---------------- e2e: host buffers through the public API
+    q_h = q.cpu().pin_memory()
+    c_h, r_h = new_c.cpu().pin_memory(), new_r.cpu().pin_memory()
+    out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    q_d, c_d, r_d = torch.empty_like(q), torch.empty_like(new_c), torch.empty_like(new_r)
+
+    def e2e_step():
+        q_d.copy_(q_h, non_blocking=True)
+        c_d.copy_(c_h, non_blocking=True)
+        r_d.copy_(r_h, non_blocking=True)
+        cache.append(c_d, r_d, block_table, seq_lens)
+        ops.mla_decode_fp8(q_d, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        ops.mla_combine(ws, B, heads_local, out, lse)
+        res = out
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
+        out_h.copy_(res, non_blocking=True)
+        lse_h.copy_(lse, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t[0])
+    h2d = q_h.numel() * 2 + c_h.numel() * 2 + r_h.numel() * 2
+    d2h = out_h.numel() * 2 + lse_h.numel() * 4
+
+    tokens_per_step = B * (world if args.mode == "dp" else 1)
+    value = tokens_per_step / (ms_step / 1e3)
+    peak, peak_src = measured_peaks()
+    kv_bytes = B * L * BYTES_PER_TOKEN
+    dec_bytes = kv_bytes + B * heads_local * 576 * 2       # algorithmic bytes per decode launch
+    achieved = dec_bytes / (dec_ms / 1e3) / 1e9
+    launches_per_step = 4   # append, plan, decode, combine (all ours)
+    res = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak" if args.mode == "dp" else "strong",
+        "vs_baseline": None,
+        "dtype": "fp8e4m3 (f32 accumulate; bf16 RoPE)",
+        "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
+        "config": {
+            "workload": w["name"], "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
+            "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": 1,
+            "parallelism": f"{args.mode}{world}",
+            "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": "mla_decode_fp8 (plan + decode launches)",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": dec_bytes, "decode_ms": round(dec_ms, 4),
+            "bytes_per_unit": f"{BYTES_PER_TOKEN} B per cached token + 1152 B per (request, head) q row",
+        },
+        "e2e": {"value": round(tokens_per_step / (e_ms / args.steps / 1e3), 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+    }
+    return res
+
+
+# -------------------------------------------------------- oracle (CPU) arms
+def oracle_request_sample(H, L, seed=0):
+    """Inputs of one request of the workload (CPU, seeded)."""
+    from paper_2602_10718_b200 import synth
+    rng = np.random.default_rng(seed)
+    c, r = synth.latent_tokens(rng, L)
+    q = synth.queries(rng, H)
+    return c.float().numpy(), r.float().numpy(), q.float().numpy()
+
+
+def oracle_step(c, r, q, scale):
+    """one decode token of one request through the oracle: append (a1) of the
+    newest token, q-quant (a2), closed-form decode (a3-a9, single split), combine."""
+    from oracle import snapmla as O
+    kc, sk, kr = O.append_quant(c, r)          # (re)quantizes the context incl. the new token
+    qc, sq, qr = O.q_quant(q)
+    o, lse = O.decode_o7(qc, sq, qr, kc, sk, kr, scale)
+    return O.combine(o[None], lse[None])
+
+
+def oracle_only_decode(kc, sk, kr, q, scale):
+    from oracle import snapmla as O
+    qc, sq, qr = O.q_quant(q)
+    o, lse = O.decode_o7(qc, sq, qr, kc, sk, kr, scale)
+    return O.combine(o[None], lse[None])
+
+
+def cpu_baseline(args, budget_s):
+    """Time the oracle as it stands on this host's cores on a bounded sample:
+    whole requests of the workload (append of the new token + q-quant + O7 +
+    combine), as many as fit in ~budget_s."""
+    from oracle import snapmla as O
+    from paper_2602_10718_b200 import synth
+    w = workload(args)
+    H, L = w["heads"], w["context"]
+    c, r, q = oracle_request_sample(H, L)
+    kc, sk, kr = O.append_quant(c[:-1], r[:-1])       # resident cache (untimed)
+    n, t_tot = 0, 0.0
+    while t_tot < budget_s:
+        t = time.perf_counter()
+        nk, ns, nr = O.append_quant(c[-1:], r[-1:])   # a1 for the new token
+        kc2, sk2, kr2 = np.concatenate([kc, nk]), np.concatenate([sk, ns]), np.concatenate([kr, nr])
+        oracle_only_decode(kc2, sk2, kr2, q, synth.DEFAULT_SOFTMAX_SCALE)
+        t_tot += time.perf_counter() - t
+        n += 1
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(n / t_tot, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} whole requests of the workload ({H} heads x {L} context): append of the new "
+                      f"token + q-quant + O7 closed-form decode + combine, numpy fp64, {t_tot:.1f} s",
+            "threads": cores}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (CPU) as the reference arm, on our config."""
+    from paper_2602_10718_b200 import synth
+    from oracle import snapmla as O
+    w = workload(args)
+    H, L = w["heads"], w["context"]
+    c, r, q = oracle_request_sample(H, L)
+    kc, sk, kr = O.append_quant(c[:-1], r[:-1])
+
+    def one():
+        nk, ns, nr = O.append_quant(c[-1:], r[-1:])
+        oracle_only_decode(np.concatenate([kc, nk]), np.concatenate([sk, ns]), np.concatenate([kr, nr]), q,
+                           synth.DEFAULT_SOFTMAX_SCALE)
+
+    for _ in range(args.warmup):
+        one()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t
+    value = args.steps / dt      # one decode token (request) per step
+    cores = len(os.sched_getaffinity(0))
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "data": "synthetic", "config": {"workload": w["name"], "batch_per_rank": w["batch"], "heads": H,
+                                        "context": L, "page": 64, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": f"each step = 1 whole request ({H} heads x {L} context) of the workload"},
+        "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/*
+ * snapmla.h -- C ABI of the B200 (sm_100a) SnapMLA FP8 MLA decode hot path.
+ *
+ * Method: SnapMLA, arXiv 2602.10718 ("P:n" = PAPER.md line n).  The library
+ * implements three calls, one per step of BASELINE.json's north_star:
+ *   mla_kv_append_quant  RoPE-aware per-token FP8 quantize-on-append (Fused-K-Append,
+ *                        §3.3; §3.1; Eq.6)
+ *   mla_decode_fp8       absorbed-MLA FP8 decode with the reconstructed PV pipeline
+ *                        (Eq.5, §3.2, Algorithm 1 P:666-744,
+ *                        Appendix C order enforcement P:759-764); Q quantization
+ *                        (Fused-Q-Quant) runs in its prologue
+ *   mla_combine          split-KV merge of the per-split (o, logsumexp) partials
+ *                        (Algorithm 1 returns o and L)
+ *
+ * Conventions (all calls)
+ *   - Every tensor pointer is a DEVICE pointer owned by the caller.  The library
+ *     never allocates, frees or synchronizes; each call only enqueues work on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Tensors are dense, row-major.  Base pointers must be 16-byte aligned; the
+ *     three KV pools must be 128-byte aligned (TMA).
+ *   - Fixed problem dims (north_star): kv_lora_rank = 512, rope_dim = 64,
+ *     page_size = 64.  Anything else returns MLA_ERR_UNSUPPORTED.
+ *   - Host-side argument errors return before anything is enqueued; launch
+ *     failures return MLA_ERR_CUDA.  No exception crosses the ABI.
+ *   - Device-side preconditions (undefined behaviour if violated): valid page
+ *     ids in block_table; 0 <= seq_lens[b] <= max_pages_per_seq * 64; KV pools
+ *     zero-initialised at allocation (stale bytes must never be FP8 NaN codes);
+ *     finite inputs; appends for a request are stream-ordered before the decode
+ *     that reads them.
+ *   - Deterministic: identical inputs on the same GPU give bitwise identical
+ *     outputs (no atomics in reductions).
+ */
+#ifndef SNAPMLA_H_
+#define SNAPMLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mla_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  MLA_OK = 0,
+  MLA_ERR_NULL = 1,        /* a required pointer is NULL                     */
+  MLA_ERR_SHAPE = 2,       /* negative / inconsistent sizes                  */
+  MLA_ERR_UNSUPPORTED = 3, /* dims outside the supported set                 */
+  MLA_ERR_ALIGN = 4,       /* pointer alignment violated                     */
+  MLA_ERR_WORKSPACE = 5,   /* workspace missing or too small                 */
+  MLA_ERR_CUDA = 6         /* CUDA runtime / driver error (launch, encode)   */
+} mla_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* mla_status_str(mla_status s);
+
+/* ABI version of this header (bumped on any signature change). */
+int mla_abi_version(void);
+
+/*
+ * mla_kv_append_quant -- quantize-on-append of one new token per request.
+ *
+ * Per request b, with the new token at position p = seq_lens[b] - 1
+ * (seq_lens is the length AFTER the append):
+ *   sigma      = max(fp32(max_i |c_kv[b,i]| / 448), 2^-24)       (content dims only)
+ *   code[i]    = E4M3_RNE_SATFINITE(fp32(c_kv[b,i] / sigma))     (IEEE division)
+ *   rope'[k]   = BF16_RNE(fp32(k_pe[b,k] / sigma))              (Eq.6 pre-scaled alignment)
+ *   slot       = block_table[b, p / 64] * 64 + p % 64
+ *   kv_fp8[slot,:] = code;  kv_rope[slot,:] = rope';  kv_scale[slot] = sigma
+ * Bit-exact with the oracle (tests/test_gpu_append.py).  Requests with
+ * seq_lens[b] <= 0 are skipped.
+ *
+ *   c_kv        bf16  [batch, kv_lora_rank]        latent of the new token
+ *   k_pe        bf16  [batch, rope_dim]            post-RoPE key of the new token
+ *   block_table int32 [batch, max_pages_per_seq]   page ids into the pools
+ *   seq_lens    int32 [batch]                      lengths after the append
+ *   kv_fp8      uint8 [num_pages, page_size, kv_lora_rank]   E4M3 codes (written)
+ *   kv_rope     bf16  [num_pages, page_size, rope_dim]       k_pe / sigma (written)
+ *   kv_scale    fp32  [num_pages, page_size]                 sigma (written)
+ */
+mla_status mla_kv_append_quant(const void* c_kv, const void* k_pe, const int32_t* block_table,
+                               const int32_t* seq_lens, int batch, int kv_lora_rank, int rope_dim,
+                               int page_size, int max_pages_per_seq, int64_t num_pages, uint8_t* kv_fp8,
+                               void* kv_rope, float* kv_scale, mla_stream_t stream);
+
+/*
+ * Workspace bytes that mla_decode_fp8 / mla_combine need for `batch` requests
+ * and `num_heads` query heads.  num_sms <= 0 means "the current device".
+ * The workspace holds the split plan and the fp32 per-split partials.
+ */
+size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms);
+
+/*
+ * mla_decode_fp8 -- absorbed-MLA FP8 decode over the paged cache, one query
+ * token per request (MTP = 1).
+ *
+ * Per request b and head h (q row = [q_nope absorbed (512) | q_pe (64)]):
+ *   sigma_q = max(fp32(amax(q[b,h,:512]) / 448), 2^-24); q codes = E4M3(q/sigma_q);
+ *   q_r'    = BF16(q_pe / sigma_q)                                      (Fused-Q-Quant)
+ *   s_j     = softmax_scale * sigma_q * sigma_K[j] * (q_codes . K_codes[j] + q_r' . k_r'[j])
+ *   per 64-token key block (aligned to token 0): online softmax, scale fusion
+ *   w_j = p_j * sigma_K[j], block-wise P quantization P' = E4M3(w * 448 / max_block w),
+ *   O <- gamma O + P' V_codes with V = the latent codes, blocks in increasing order.
+ * Result (through mla_combine): o = softmax-weighted latent (512), natural-log LSE.
+ * Writes only the workspace (split plan + fp32 partials); call mla_combine next.
+ *
+ *   q             bf16  [batch, num_heads, 576]
+ *   kv_*          the pools written by mla_kv_append_quant (read only)
+ *   block_table   int32 [batch, max_pages_per_seq];  seq_lens int32 [batch]
+ *   num_heads     1..128 (processed in 64-row head tiles; H < 64 is zero-padded)
+ *   softmax_scale multiplies the dequantized logit (e.g. 1/sqrt(192) * mscale^2)
+ *   workspace     device buffer of >= mla_decode_workspace_bytes(batch, num_heads, 0)
+ */
+mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const void* kv_rope, const float* kv_scale,
+                          const int32_t* block_table, const int32_t* seq_lens, int batch, int num_heads,
+                          int kv_lora_rank, int rope_dim, int page_size, int max_pages_per_seq,
+                          int64_t num_pages, float softmax_scale, void* workspace, size_t workspace_bytes,
+                          mla_stream_t stream);
+
+/*
+ * mla_combine -- merge split-KV partials left in `workspace` by the preceding
+ * mla_decode_fp8 (same batch / num_heads, stream-ordered):
+ *   L = log sum_s e^{L_s};   o = sum_s e^{L_s - L} o_s
+ *   out  bf16 [batch, num_heads, kv_lora_rank]  (RNE from fp32)
+ *   lse  fp32 [batch, num_heads], natural log; may be NULL
+ * A request with seq_lens[b] == 0 yields out = 0 and lse = -inf.
+ */
+mla_status mla_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out, float* lse,
+                       mla_stream_t stream);
+
+/* Same as mla_combine but writes fp32 output [batch, num_heads, kv_lora_rank]
+ * (diagnostic: exposes the kernel result before the final BF16 rounding). */
+mla_status mla_combine_f32(const void* workspace, int batch, int num_heads, int kv_lora_rank, float* out,
+                           float* lse, mla_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNAPMLA_H_ */

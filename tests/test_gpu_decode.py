@@ -1,0 +1,131 @@
+"""a2-a10 parity: CUDA FP8 decode (+ combine) vs the oracle's closed form O7.
+
+Gate (BASELINE.json north_star, reading R23 in DESIGN.md): max-abs <= 2e-2 * RMS
+and mean-abs <= 2e-3 * RMS of the O7 output over the checked rows, applied to
+  * the fp32 kernel result (mla_combine_f32), and
+  * the BF16 output, whose max-abs allowance adds the BF16 output rounding
+    itself (RNE to an 8-bit significand: <= 2^-8 |o7| per element): with max|o|/RMS ~ 12 on the
+    MLA-like latent, RNE to BF16 alone moves an element by up to ~4.7e-2 * RMS.
+The BF16 output must also equal RNE(fp32 output) bit for bit.
+Diagnostic (tight) on the fp32 result: max-abs <= 1e-3 * RMS.  LSE within 1e-3.
+Errors vs O6 (exact softmax over the dequantized cache) and O8 (unquantized
+BF16 MLA) are printed, not gated (reading R22).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_cases import Case, parity_stats
+from oracle import snapmla as O
+
+pytestmark = pytest.mark.gpu
+
+GATE_MAX, GATE_MEAN, DIAG_MAX, LSE_ABS = 2e-2, 2e-3, 1e-3, 1e-3
+
+
+def _check(case, heads_per_req=None, report=False):
+    cache = case.gpu_cache()
+    out, lse = case.gpu_decode(cache)
+    out32, lse32 = case.gpu_decode(cache, f32_out=True)
+    pools = case.oracle_pools()
+    refs, gots, gots32, lref, lgot = [], [], [], [], []
+    for b in range(case.B):
+        if case.lens[b] == 0:
+            continue
+        hs = np.arange(case.H) if heads_per_req is None else heads_per_req
+        o7, l7 = case.oracle_request(pools, b, heads=hs)
+        refs.append(o7)
+        gots.append(out[b, hs])
+        gots32.append(out32[b, hs])
+        lref.append(l7)
+        lgot.append(lse[b, hs])
+    ref = np.concatenate(refs)
+    got, got32 = np.concatenate(gots), np.concatenate(gots32)
+    rms = float(np.sqrt(np.mean(ref ** 2)))
+    excess = np.abs(got - ref) - 2.0 ** -8 * np.abs(ref)       # beyond BF16 output rounding (unit roundoff 2^-8)
+    mx = float(excess.max() / rms)
+    _, mn = parity_stats(got, ref)
+    mx32, mn32 = parity_stats(got32, ref)
+    rne = torch.from_numpy(got32.astype(np.float32)).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(rne, got), "bf16 output is not RNE(fp32 output)"
+    lerr = float(np.max(np.abs(np.concatenate(lgot) - np.concatenate(lref))))
+    msg = (f"bf16 (max-abs - bf16 half-ulp)/rms={mx:.2e} mean/rms={mn:.2e} | f32 max/rms={mx32:.2e} "
+           f"mean/rms={mn32:.2e} | lse={lerr:.2e}")
+    if report:
+        b = int(np.argmax(case.lens))
+        o6, _ = case.oracle_request(pools, b, which="o6")
+        o8, _ = case.oracle_request(pools, b, which="o8")
+        msg += f" | vs O6 {O.error_metrics(out[b], o6)} | vs O8 {O.error_metrics(out[b], o8)}"
+    print(msg)
+    assert mx <= GATE_MAX and mn <= GATE_MEAN, msg
+    assert mx32 <= GATE_MAX and mn32 <= GATE_MEAN, msg
+    assert mx32 <= DIAG_MAX, msg
+    assert lerr <= LSE_ABS, msg
+    return out, lse
+
+
+def test_tiny_config():
+    """BASELINE.json configs[0]: batch 1, 16 heads, context 256."""
+    _check(Case([256], 16, seed=0), report=True)
+
+
+@pytest.mark.parametrize("L", [1, 2, 63, 64, 65, 127, 128, 129, 4096 + 17])
+def test_seq_len_sweep(L):
+    _check(Case([L], 16, seed=L))
+
+
+@pytest.mark.parametrize("H", [16, 32, 64, 128])
+def test_head_counts(H):
+    _check(Case([700, 64, 1, 2049], H, seed=H))
+
+
+@pytest.mark.parametrize("dist", ["mla", "iid"])
+def test_variable_lengths_many_requests(dist):
+    rng = np.random.default_rng(11)
+    lens = rng.integers(1, 2500, 37)
+    _check(Case(lens, 64, seed=12, dist=dist), heads_per_req=np.array([0, 17, 63]))
+
+
+def test_splits_many_ctas_single_request():
+    """one long request is split across all CTAs; block-aligned splits + LSE combine."""
+    _check(Case([148 * 64 * 3 + 5], 128, seed=13), heads_per_req=np.array([0, 1, 64, 127]))
+
+
+def test_zero_length_request():
+    case = Case([0, 100, 0, 65], 16, seed=14)
+    out, lse = _check(case)
+    assert np.all(out[0] == 0) and np.all(out[2] == 0)
+    assert np.all(np.isneginf(lse[0])) and np.all(np.isneginf(lse[2]))
+
+
+def test_single_token_is_v_deq():
+    case = Case([1, 1], 32, seed=15)
+    cache = case.gpu_cache()
+    out32, lse32 = case.gpu_decode(cache, f32_out=True)
+    pools = case.oracle_pools()
+    for b in range(2):
+        kc, sk, _ = O.gather_request(pools, case.bt[b], 1)
+        v = O.decode_e4m3(kc[0]) * np.float64(sk[0])
+        np.testing.assert_allclose(out32[b], np.broadcast_to(v, (32, 512)), rtol=2e-6, atol=1e-30)
+
+
+def test_duplicated_tokens_lse_plus_ln2():
+    case1 = Case([1], 16, seed=16)
+    case2 = Case([2], 16, seed=16)
+    case2.c_kv = case1.c_kv.repeat(2, 1)
+    case2.k_pe = case1.k_pe.repeat(2, 1)
+    case2.q = case1.q
+    _, l1 = case1.gpu_decode(case1.gpu_cache(), f32_out=True)
+    _, l2 = case2.gpu_decode(case2.gpu_cache(), f32_out=True)
+    np.testing.assert_allclose(l2, l1 + math.log(2.0), atol=1e-5)
+
+
+def test_deterministic_bitwise():
+    case = Case([3000, 17, 900], 64, seed=17)
+    cache = case.gpu_cache()
+    o1, l1 = case.gpu_decode(cache, f32_out=True)
+    o2, l2 = case.gpu_decode(cache, f32_out=True)
+    assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
+    assert np.array_equal(l1.view(np.uint32), l2.view(np.uint32))
