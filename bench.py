@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--quick", action="store_true",
+                    help="profiling runs: no clock-settle loop, no e2e leg, no cpu baseline")
     return ap.parse_args()
 
 
@@ -194,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     t_settle = time.time()
-    while time.time() - t_settle < 1.0:        # keep the GPU loaded so clocks are sampled under load
+    while not args.quick and time.time() - t_settle < 1.0:        # keep the GPU loaded so clocks are sampled under load
         for _ in range(10):
             step()
         torch.cuda.synchronize()
@@ -218,6 +220,10 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, dec_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
+
+    if args.quick:
+        return {"metric": METRIC, "value": round(B * (world if args.mode == "dp" else 1) / (ms_step / 1e3), 1),
+                "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True}
 
     # ---------------- e2e: host buffers through the public API
     q_h = q.cpu().pin_memory()
@@ -399,7 +405,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         res["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(res))

@@ -6,36 +6,40 @@
 // with Appendix C's strictly monotonic accumulation order.
 //
 // B200 design: one persistent CTA per SM, one 64-row query-head
-// tile per CTA (UMMA M = 64), split-KV over 64-token blocks planned on the
-// device.  Warp roles:
-//   warp 0     TMA producer: paged KV tiles (4 x 8 KB FP8 boxes + 8 KB BF16
-//              RoPE box, SWIZZLE_128B) + 256 B scales (bulk copy), 4-stage ring
-//   warp 1     TMEM owner + single-thread tcgen05.mma issuer:
-//                QK: 16 x kind::f8f6f4 (K=32) + 4 x kind::f16 (K=16) into ONE
-//                    fp32 accumulator S (Eq.6 makes the domains agree)
-//                PV: P' (SMEM, K-major) x V (the SAME FP8 tile read MN-major:
-//                    no transpose) into O (TMEM, 64 x 512 fp32)
-//   warps 2-5  Q-quant prologue (Fused-Q-Quant), online softmax, scale fusion,
-//              block P quantization, O rescale by gamma, epilogue.
+// tile per CTA (UMMA M = 64), split-KV over 64-token key blocks planned on the
+// device, a 4-slot ring of 64-token KV blocks in SMEM.  Warp roles (13 warps):
+//   warp 0       TMA producer: per block 4 x 8 KB FP8 boxes + 8 KB BF16 RoPE box
+//                (SWIZZLE_128B, row coordinate from the block table) + 256 B scales
+//   warps 1, 2   QK issuers for even / odd blocks (warp 1 also owns TMEM):
+//                16 x kind::f8f6f4 (K=32) + 4 x kind::f16 (K=16) into ONE fp32
+//                accumulator S (Eq.6 makes the two domains agree)
+//   warps 3, 4   PV_L / PV_R issuers: P' (SMEM, K-major) x V (the SAME FP8 tile
+//                read MN-major: no transpose) into O_L / O_R
+//   warps 5-8    Q-quant prologue (Fused-Q-Quant), online softmax, scale fusion,
+//                block P quantization; thread = (head row, 32-token half)
+//   warps 9-12   correction O_L / O_R <- gamma O in TMEM, epilogue (fp32 partials)
+// Issue warps run converged and elect one lane per tcgen05 op.  Measured on
+// B200 (scripts/mma_bench.cu): a tcgen05.commit stalls the issuing warp's next
+// MMA until completion, so every MMA stream that commits gets its own warp and
+// the streams overlap in the tensor pipe.
 // TMEM (512 cols): O in the lower half-subpartitions (lanes 0-15 of each 32),
-// two S buffers in the upper half-subpartitions (lanes 16-31), cols 0-63 / 64-127.
+// four S buffers (64 cols each) in the upper half-subpartitions (lanes 16-31).
 #include "snapmla_internal.h"
 
 namespace snapmla {
 
-constexpr int kStages = 4;
-constexpr int kThreads = 192;
-constexpr uint32_t kKvContent = kBc * kDc;      // 32768 B
-constexpr uint32_t kKvRope = kBc * kDr * 2;     // 8192 B
-constexpr uint32_t kKvScale = kBc * 4;          // 256 B
-constexpr uint32_t kKvTx = kKvContent + kKvRope + kKvScale;   // 41216 B per block
-constexpr uint32_t kStageBytes = 41984;         // kKvTx rounded up to 1024
-constexpr uint32_t kOffQc = 0;                  // 4 x [64 rows x 128 B] SW128
-constexpr uint32_t kOffQr = 32768;              // [64 rows x 128 B] SW128
-constexpr uint32_t kOffP = 40960;               // 2 x 4096 B, no swizzle, K-major core matrices
-constexpr uint32_t kOffKv = 49152;
-constexpr uint32_t kOffBar = kOffKv + kStages * kStageBytes;
-constexpr uint32_t kSmemBytes = kOffBar + 256 + 1024;   // + alignment slack
+constexpr int kThreads = 416;   // 13 warps
+constexpr int kSlots = 4;       // KV / S / P' ring depth (blocks)
+constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
+constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
+constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
+constexpr uint32_t kOffQc = 0;                              // 4 x [64 rows x 128 B] SW128
+constexpr uint32_t kOffQr = 32768;                          // [64 rows x 128 B] SW128
+constexpr uint32_t kOffP = 40960;                           // 4 slots x 4096 B, K-major core matrices
+constexpr uint32_t kOffKv = 57344;                          // 4 slots: 4 content boxes | RoPE box | scales
+constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
+constexpr uint32_t kSmemBytes = kOffBar + 3072 + 1024;      // barriers/gamma/stats + alignment slack
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 // instruction descriptors (M = 64)
 constexpr uint32_t kIdescQk8 = make_idesc(0, 0, 0, 0, 64, 64);      // E4M3 x E4M3, both K-major
@@ -54,14 +58,30 @@ struct DecodeParams {
   float* o_part;
   int batch, num_heads, n_ht, max_pages;
   float scale_log2;   // softmax_scale * log2(e)
+  unsigned long long* trace;   // debug timeline (CTA 0), nullptr in production
 };
 
+// debug timeline: trace[ev * kTraceN + n] = clock64() of event ev at block n (CTA 0 only)
+constexpr int kTraceN = 256;
+enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, TR_C_R, TR_NEV };
+#define TRACE(ev, n)                                                                          \
+  do {                                                                                        \
+    if (p.trace != nullptr && blockIdx.x == 0 && (n) < (uint32_t)kTraceN)                     \
+      p.trace[(ev) * kTraceN + (n)] = clock64();                                              \
+  } while (0)
+
 struct Bars {
-  uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[2], s_empty[2], p_full[2];
-  uint64_t o_done, q_full;
+  uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
+  uint64_t s_full[kSlots], s_empty[kSlots];     // QK -> softmax / softmax -> QK
+  uint64_t p_full[kSlots], p_empty[kSlots];     // P', gamma: softmax -> PV + correction / PV_L + PV_R -> softmax
+  uint64_t oL_ready, oR_ready, oL_done, oR_done;   // correction <-> PV halves
+  uint64_t q_full;                    // Q-quant prologue -> QK
+  uint64_t st_full[2], st_empty[2];   // per-unit epilogue factors softmax -> correction
   uint32_t tmem_base;
+  float gamma[kSlots][64];
+  float stat[2][64][2];
 };
+static_assert(sizeof(Bars) <= 3072, "barrier region");
 
 // ------------------------------------------------------------------ plan (a3)
 // One CTA.  cum[b] = sum_{b'<b} ceil(L_b'/64) (exclusive scan), total T.
@@ -74,8 +94,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
                                                     int groups, int32_t* __restrict__ hdr,
                                                     int32_t* __restrict__ cum, int32_t* __restrict__ first_req) {
   __shared__ int warp_sums[32];
-  __shared__ int s_per, s_total;
+  __shared__ int s_per;
   const int tid = threadIdx.x;
+  pdl_launch_dependents();
   const int per_thr = (batch + 1023) / 1024;
   const int b0 = tid * per_thr;
   int local = 0;
@@ -120,7 +141,6 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
     cum[batch] = total;
     const int per = total > 0 ? (total + groups - 1) / groups : 1;
     s_per = per;
-    s_total = total;
     hdr[H_TOTAL] = total;
     hdr[H_PER] = per;
     hdr[H_GROUPS] = groups;
@@ -139,10 +159,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
     const int c1 = c0 + (L > 0 ? (L + kBc - 1) / kBc : 0);
     for (int g = (c0 + per - 1) / per; g < groups && g * per < c1; ++g) first_req[g] = b;
   }
-  (void)s_total;
 }
 
-// ------------------------------------------------------------ unit iteration
+// ------------------------------------------------------------------- units
 struct Unit {
   int b, k0, k1, slot;
 };
@@ -169,6 +188,41 @@ struct UnitIter {
 };
 
 // ------------------------------------------------------------- decode kernel
+// O <- gamma O on 16 lanes x 256 columns (threads 0-15 [c, c+32), 16-31 [c+128, c+160))
+__device__ __forceinline__ void rescale_half(uint32_t taddr, float gamma) {
+  const float2 g2 = make_float2(gamma, gamma);
+#pragma unroll
+  for (int c = 0; c < 128; c += 64) {
+    uint32_t v0[32], v1[32];
+    tmem_ld_16x32bx2_x32<128>(taddr + c, v0);
+    tmem_ld_16x32bx2_x32<128>(taddr + c + 32, v1);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      float2 a = __fmul2_rn(make_float2(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])), g2);
+      v0[i] = __float_as_uint(a.x);
+      v0[i + 1] = __float_as_uint(a.y);
+      a = __fmul2_rn(make_float2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1])), g2);
+      v1[i] = __float_as_uint(a.x);
+      v1[i + 1] = __float_as_uint(a.y);
+    }
+    tmem_st_16x32bx2_x32<128>(taddr + c, v0);
+    tmem_st_16x32bx2_x32<128>(taddr + c + 32, v1);
+  }
+  tmem_wait_st();
+}
+
+// x / s for a row-constant s: rcp + one Newton/FMA correction of the quotient
+// (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
+__device__ __forceinline__ float div_by(float x, float s, float rs) {
+  const float q = x * rs;
+  return fmaf(fmaf(-q, s, x), rs, q);
+}
+
+__device__ __forceinline__ uint32_t cvt4_e4m3(float a, float b, float c, float d) {
+  return (uint32_t)cvt_e4m3x2(a, b) | ((uint32_t)cvt_e4m3x2(c, d) << 16);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
                       const DecodeParams p) {
@@ -178,24 +232,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int ht = blockIdx.x % p.n_ht;
-  const int g = blockIdx.x / p.n_ht;
-  const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
-  const int lo = g * per;
-  if (g >= groups || lo >= total) return;   // uniform per CTA: no work
-  const int hi = min(total, lo + per);
-
+  // ---- setup overlaps the plan kernel (programmatic dependent launch)
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       mbar_init(&bars.kv_full[i], 1);
-      mbar_init(&bars.kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.kv_empty[i], 2);
       mbar_init(&bars.s_full[i], 1);
       mbar_init(&bars.s_empty[i], 128);
       mbar_init(&bars.p_full[i], 128);
+      mbar_init(&bars.p_empty[i], 2);
     }
-    mbar_init(&bars.o_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.st_full[i], 128);
+      mbar_init(&bars.st_empty[i], 128);
+    }
+    mbar_init(&bars.oL_ready, 128);
+    mbar_init(&bars.oR_ready, 128);
+    mbar_init(&bars.oL_done, 1);
+    mbar_init(&bars.oR_done, 1);
     mbar_init(&bars.q_full, 128);
     fence_barrier_init();
   }
@@ -208,10 +262,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-  const uint32_t tmem_O = tmem;                       // lanes 0-15 (+32k), cols 0..511
-  const uint32_t tmem_S = tmem + (16u << 16);         // lanes 16-31 (+32k), cols 64*buf
+  const uint32_t tmem_O = tmem;                       // lanes 0-15 (+32k): O_L cols 0-255, O_R 256-511
+  const uint32_t tmem_S = tmem + (16u << 16);         // lanes 16-31 (+32k): S slot s at cols 64 s
 
-  UnitIter it{p.cum, lo, hi, g, __ldg(p.first_req + g), p.batch};
+  pdl_wait();   // plan (and the appends before it) visible from here on
+  const int ht = blockIdx.x % p.n_ht;
+  const int g = blockIdx.x / p.n_ht;
+  const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
+  const int lo = g * per;
+  const bool has_work = g < groups && lo < total;
+  const int hi = min(total, lo + per);
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x] = gt;
+  }
+
+  UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
   Unit u;
 
   if (warp == 0) {
@@ -222,89 +289,99 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (it.next(u)) {
         const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
         for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kStages;
-          mbar_wait(&bars.kv_empty[st], ((n / kStages) & 1) ^ 1);
-          const int page = __ldg(bt + j);
-          const int row = page * kPage;
-          const uint32_t dst = sbase + kOffKv + st * kStageBytes;
+          const uint32_t st = n % kSlots;
+          mbar_wait(&bars.kv_empty[st], ((n / kSlots) & 1) ^ 1);
+          TRACE(TR_TMA, n);
+          const int row = __ldg(bt + j) * kPage;
+          const uint32_t dst = sbase + kOffKv + st * kStage;
           mbar_arrive_expect_tx(&bars.kv_full[st], kKvTx);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * 8192, &tm_kv, &bars.kv_full[st], c * 128, row, pol);
-          tma_load_2d(dst + kKvContent, &tm_rope, &bars.kv_full[st], 0, row, pol);
-          bulk_load(dst + kKvContent + kKvRope, p.kv_scale + (int64_t)row, kKvScale, &bars.kv_full[st], pol);
+          for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, &bars.kv_full[st], c * 128, row, pol);
+          tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, &bars.kv_full[st], 0, row, pol);
+          bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, &bars.kv_full[st], pol);
         }
       }
     }
-  } else if (warp == 1) {
-    // ============================= MMA issuer =============================
-    if (lane == 0) {
-      uint32_t n = 0, unit = 0;
-      auto issue_pv = [&](uint32_t k, bool first) {
-        mbar_wait(&bars.p_full[k & 1], (k >> 1) & 1);
+  } else if (warp <= 2) {
+    // =================== QK issuers (warp 1: even blocks, warp 2: odd) ===================
+    const uint32_t parity = warp - 1;
+    uint32_t n = 0, unit = 0;
+    while (it.next(u)) {
+      mbar_wait(&bars.q_full, unit & 1);
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        if ((n & 1) != parity) continue;
+        const uint32_t st = n % kSlots;
+        mbar_wait(&bars.kv_full[st], (n / kSlots) & 1);
+        mbar_wait(&bars.s_empty[st], ((n / kSlots) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t pA = sbase + kOffP + (k & 1) * 4096;
-        const uint32_t kv = sbase + kOffKv + (k % kStages) * kStageBytes;
+        if (lane == 0) TRACE(TR_QK, n);
+        const uint32_t kv = sbase + kOffKv + st * kStage;
+        const uint32_t dS = tmem_S + 64 * st;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t a = make_smem_desc(pA + ks * 2048, 1024, 128, LAYOUT_NONE);
-            const uint64_t bdesc = make_smem_desc(kv + (2 * h) * 8192 + ks * 4096, 8192, 1024, LAYOUT_SW128);
-            mma_f8(tmem_O + 256 * h, a, bdesc, kIdescPv, (first && ks == 0) ? 0u : 1u);
-          }
+        for (int kk = 0; kk < 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          mma_f8_ws(dS, make_smem_desc(sbase + kOffQc + off, 16, 1024, LAYOUT_SW128),
+                    make_smem_desc(kv + off, 16, 1024, LAYOUT_SW128), kIdescQk8, kk > 0);
         }
-        mma_commit(&bars.kv_empty[k % kStages]);
-        mma_commit(&bars.o_done);
-      };
-      while (it.next(u)) {
-        mbar_wait(&bars.q_full, unit & 1);
+#pragma unroll
+        for (int kr = 0; kr < 4; ++kr) {
+          mma_bf16_ws(dS, make_smem_desc(sbase + kOffQr + kr * 32, 16, 1024, LAYOUT_SW128),
+                      make_smem_desc(kv + 4 * kBoxBytes + kr * 32, 16, 1024, LAYOUT_SW128), kIdescQk16, 1u);
+        }
+        mma_commit_ws(&bars.s_full[st]);
+      }
+      ++unit;
+    }
+  } else if (warp <= 4) {
+    // ========================= PV_L (warp 3) / PV_R (warp 4) =========================
+    const uint32_t half = warp - 3;
+    uint64_t* ready = half == 0 ? &bars.oL_ready : &bars.oR_ready;
+    uint64_t* done = half == 0 ? &bars.oL_done : &bars.oR_done;
+    uint32_t n = 0;
+    while (it.next(u)) {
+      const uint32_t n0 = n;
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        const uint32_t st = n % kSlots;
+        mbar_wait(&bars.p_full[st], (n / kSlots) & 1);    // P'(n) in SMEM
+        mbar_wait(ready, n & 1);                          // O half rescaled by gamma(n)
         tc_fence_after();
-        const uint32_t n0 = n;
-        for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kStages;
-          mbar_wait(&bars.kv_full[st], (n / kStages) & 1);
-          mbar_wait(&bars.s_empty[n & 1], ((n >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t kv = sbase + kOffKv + st * kStageBytes;
-          const uint32_t dS = tmem_S + 64 * (n & 1);
+        if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+        const uint32_t pA = sbase + kOffP + st * 4096;
+        const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
-            mma_f8(dS, make_smem_desc(sbase + kOffQc + off, 16, 1024, LAYOUT_SW128),
-                   make_smem_desc(kv + off, 16, 1024, LAYOUT_SW128), kIdescQk8, kk > 0);
-          }
-#pragma unroll
-          for (int kr = 0; kr < 4; ++kr) {
-            mma_bf16(dS, make_smem_desc(sbase + kOffQr + kr * 32, 16, 1024, LAYOUT_SW128),
-                     make_smem_desc(kv + kKvContent + kr * 32, 16, 1024, LAYOUT_SW128), kIdescQk16, 1u);
-          }
-          mma_commit(&bars.s_full[n & 1]);
-          if (n > n0) issue_pv(n - 1, n - 1 == n0);
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t a = make_smem_desc(pA + ks * 2048, 1024, 128, LAYOUT_NONE);
+          const uint64_t b = make_smem_desc(vb + ks * 4096, kBoxBytes, 1024, LAYOUT_SW128);
+          mma_f8_ws(tmem_O + 256 * half, a, b, kIdescPv, (n == n0 && ks == 0) ? 0u : 1u);
         }
-        issue_pv(n - 1, n - 1 == n0);
-        ++unit;
+        mma_commit_ws(done);
+        mma_commit_ws(&bars.p_empty[st]);
+        mma_commit_ws(&bars.kv_empty[st]);
       }
     }
-  } else {
-    // =================== softmax / quant / correction (128 thr) ===================
+  } else if (warp <= 8) {
+    // ====== softmax / scale fusion / P quantization (warps 5-8): thread = (row, token half) ======
     const int k = warp & 3;                  // TMEM subpartition of this warp
-    const int t = lane & 15, h = lane >> 4;  // row-in-quarter, token half
+    const int t = lane & 15, h = lane >> 4;  // row-in-quarter, 32-token half
     const int r = 16 * k + t;                // query-head row inside the tile
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    uint32_t n = 0;
+    uint32_t n = 0, unit = 0;
     while (it.next(u)) {
-      // ---------------- Fused-Q-Quant prologue (a2)
+      // ---------------- Fused-Q-Quant prologue (a2): row r, content half h
       float c_row;
       {
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
         float amax = 0.f;
-        if (row_ok) {
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i) {
-            const uint4 v = __ldg(qrow + 32 * h + i);
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int bh = 0; bh < 2; ++bh) {
+          uint4 qv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * h + 16 * bh + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(hv[e]);
@@ -314,44 +391,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
+        const float rsq = __frcp_rn(sq);
         c_row = sq * p.scale_log2;
         uint8_t* qc = smem + kOffQc;
 #pragma unroll 4
-        for (int gch = 0; gch < 16; ++gch) {   // 16-byte chunk of codes
-          uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-          if (row_ok) {
-            v0 = __ldg(qrow + 32 * h + 2 * gch);
-            v1 = __ldg(qrow + 32 * h + 2 * gch + 1);
-          }
-          const __nv_bfloat162* a0 = reinterpret_cast<const __nv_bfloat162*>(&v0);
-          const __nv_bfloat162* a1 = reinterpret_cast<const __nv_bfloat162*>(&v1);
+        for (int gch = 0; gch < 16; ++gch) {   // 16-byte chunk of codes (re-read: L1 hit)
+          uint4 v[2];
+          v[0] = row_ok ? __ldg(qrow + 32 * h + 2 * gch) : make_uint4(0, 0, 0, 0);
+          v[1] = row_ok ? __ldg(qrow + 32 * h + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v);
           uint32_t w[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float2 f0 = __bfloat1622float2(a0[2 * e]), f1 = __bfloat1622float2(a0[2 * e + 1]);
-            w[e] = (uint32_t)cvt_e4m3x2(__fdiv_rn(f0.x, sq), __fdiv_rn(f0.y, sq)) |
-                   ((uint32_t)cvt_e4m3x2(__fdiv_rn(f1.x, sq), __fdiv_rn(f1.y, sq)) << 16);
-            const float2 g0 = __bfloat1622float2(a1[2 * e]), g1 = __bfloat1622float2(a1[2 * e + 1]);
-            w[2 + e] = (uint32_t)cvt_e4m3x2(__fdiv_rn(g0.x, sq), __fdiv_rn(g0.y, sq)) |
-                       ((uint32_t)cvt_e4m3x2(__fdiv_rn(g1.x, sq), __fdiv_rn(g1.y, sq)) << 16);
+          for (int e = 0; e < 4; ++e) {
+            const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+            w[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                             div_by(f1.y, sq, rsq));
           }
           const int byte = 256 * h + 16 * gch;          // byte offset inside the 512-B row
           const int sub = byte >> 7, c = (byte >> 4) & 7;
-          *reinterpret_cast<uint4*>(qc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4)) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(qc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         uint8_t* qr = smem + kOffQr;
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (row_ok) v = __ldg(qrow + 64 + 4 * h + gch);
+          const uint4 v = row_ok ? __ldg(qrow + 64 + 4 * h + gch) : make_uint4(0, 0, 0, 0);
           const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = __bfloat1622float2(a[e]);
-            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(__fdiv_rn(f.x, sq)),
-                                                   __float2bfloat16_rn(__fdiv_rn(f.y, sq)));
+            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
+                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
             w[e] = *reinterpret_cast<uint32_t*>(&o2);
           }
           const int c = 4 * h + gch;
@@ -362,34 +432,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 
       const int L = __ldg(p.seq_lens + u.b);
-      float m_run = -INFINITY;   // running max of t = S * sigma_K (units of the descaled logit / (sigma_q*scale))
+      float m_run = -INFINITY;   // running max of t = S * sigma_K (Alg.1 m)
       float l_part = 0.f;        // this thread's partial of l = sum_j 2^{(t_j - m) c}
       float sigma_p = 1.0f;      // Alg.1 line 1
-      const uint32_t n0 = n;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t buf = n & 1;
-        mbar_wait(&bars.s_full[buf], (n >> 1) & 1);
+        const uint32_t st = n % kSlots;
+        mbar_wait(&bars.s_full[st], (n / kSlots) & 1);
         tc_fence_after();
-        uint32_t sr[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_base + 64 * buf, sr);
+        if (threadIdx.x == 160) TRACE(TR_SM_IN, n);
+        float tt[32];
+        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_base + 64 * st, *reinterpret_cast<uint32_t(*)[32]>(tt));
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&bars.s_empty[buf]);
+        mbar_arrive(&bars.s_empty[st]);
 
-        // sigma_K of my 32 tokens (from the TMA'd stage)
-        const float* sk = reinterpret_cast<const float*>(smem + kOffKv + (n % kStages) * kStageBytes + kKvContent +
-                                                         kKvRope) + 32 * h;
-        const int tok0 = j * kBc + 32 * h;
-        const int nvalid = min(32, L - tok0);
-        float tt[32];
+        // sigma_K of my 32 tokens (from the TMA'd slot)
+        const float* sk = reinterpret_cast<const float*>(smem + kOffKv + st * kStage + 5 * kBoxBytes) + 32 * h;
+        const int nvalid = min(32, L - (j * kBc + 32 * h));
         float mx = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 s4 = *reinterpret_cast<const float4*>(sk + i);
-          tt[i + 0] = (i + 0 < nvalid) ? __uint_as_float(sr[i + 0]) * s4.x : -INFINITY;   // Alg.1 step 3
-          tt[i + 1] = (i + 1 < nvalid) ? __uint_as_float(sr[i + 1]) * s4.y : -INFINITY;
-          tt[i + 2] = (i + 2 < nvalid) ? __uint_as_float(sr[i + 2]) * s4.z : -INFINITY;
-          tt[i + 3] = (i + 3 < nvalid) ? __uint_as_float(sr[i + 3]) * s4.w : -INFINITY;
+          tt[i + 0] = (i + 0 < nvalid) ? tt[i + 0] * s4.x : -INFINITY;   // Alg.1 step 3
+          tt[i + 1] = (i + 1 < nvalid) ? tt[i + 1] * s4.y : -INFINITY;
+          tt[i + 2] = (i + 2 < nvalid) ? tt[i + 2] * s4.z : -INFINITY;
+          tt[i + 3] = (i + 3 < nvalid) ? tt[i + 3] * s4.w : -INFINITY;
           mx = fmaxf(mx, fmaxf(fmaxf(tt[i], tt[i + 1]), fmaxf(tt[i + 2], tt[i + 3])));
         }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
@@ -417,58 +484,92 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float gamma = alpha * __fdiv_rn(sigma_p, sp_new);        // step 9
         uint32_t pw[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          pw[i] = (uint32_t)cvt_e4m3x2(tt[4 * i] * inv, tt[4 * i + 1] * inv) |
-                  ((uint32_t)cvt_e4m3x2(tt[4 * i + 2] * inv, tt[4 * i + 3] * inv) << 16);
-        }
-        // P' tile: K-major core matrices; byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
-        uint8_t* pdst = smem + kOffP + buf * 4096 + r * 16;
+        for (int i = 0; i < 8; ++i)
+          pw[i] = cvt4_e4m3(tt[4 * i] * inv, tt[4 * i + 1] * inv, tt[4 * i + 2] * inv, tt[4 * i + 3] * inv);
+        // P' slot free once PV_L and PV_R of block n - kSlots completed
+        mbar_wait(&bars.p_empty[st], ((n / kSlots) & 1) ^ 1);
+        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
+        uint8_t* pdst = smem + kOffP + st * 4096 + r * 16;
         *reinterpret_cast<uint4*>(pdst + (2 * h) * 1024) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
         *reinterpret_cast<uint4*>(pdst + (2 * h + 1) * 1024) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+        if (h == 0) bars.gamma[st][r] = gamma;
         fence_proxy_async_smem();
-
-        // O <- gamma * O before P'V of this block is accumulated (steps 10/17, monotonic order)
-        if (n != n0) {
-          mbar_wait(&bars.o_done, (n - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < 256; c += 32) {
-            uint32_t ov[32];
-            tmem_ld_16x32bx2_x32<256>(tmem_O + lane_base + c, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * gamma);
-            tmem_st_16x32bx2_x32<256>(tmem_O + lane_base + c, ov);
-          }
-          tmem_wait_st();
-        }
-        tc_fence_before();
-        mbar_arrive(&bars.p_full[buf]);
+        mbar_arrive(&bars.p_full[st]);
+        if (threadIdx.x == 160) TRACE(TR_SM_OUT, n);
         m_run = m_new;
         sigma_p = sp_new;
       }
-
-      // ---------------- epilogue (a9): o = sigma_p * O / l ; L = m + ln(sigma_p l)
-      mbar_wait(&bars.o_done, (n - 1) & 1);
-      tc_fence_after();
+      // per-row epilogue factors (a9): o = sigma_p * O / l ; L = (m c + log2 l) ln 2
       const float l_tot = l_part + __shfl_xor_sync(0xffffffffu, l_part, 16);
-      const float f = sigma_p / l_tot;
+      const uint32_t sb = unit & 1;
+      mbar_wait(&bars.st_empty[sb], ((unit >> 1) & 1) ^ 1);
+      if (h == 0) {
+        bars.stat[sb][r][0] = sigma_p / l_tot;
+        bars.stat[sb][r][1] = (m_run * c_row + log2f(l_tot)) * 0.69314718055994531f;
+      }
+      mbar_arrive(&bars.st_full[sb]);
+      ++unit;
+    }
+  } else {
+    // ============ correction + epilogue (warps 9-12): O <- gamma O ============
+    const int k = warp & 3;
+    const int t = lane & 15, h = lane >> 4;
+    const int r = 16 * k + t;
+    const int head = ht * kHeadTile + r;
+    const bool row_ok = head < p.num_heads;
+    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
+    uint32_t n = 0, unit = 0;
+    while (it.next(u)) {
+      const uint32_t n0 = n;
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        if (n != n0) {
+          const uint32_t st = n % kSlots;
+          mbar_wait(&bars.p_full[st], (n / kSlots) & 1);
+          const float gamma = bars.gamma[st][r];
+          mbar_wait(&bars.oL_done, (n - 1) & 1);
+          tc_fence_after();
+          rescale_half(tmem_O + lane_base, gamma);
+          tc_fence_before();
+          mbar_arrive(&bars.oL_ready);
+          if (threadIdx.x == 288) TRACE(TR_C_L, n);
+          mbar_wait(&bars.oR_done, (n - 1) & 1);
+          tc_fence_after();
+          rescale_half(tmem_O + lane_base + 256, gamma);
+          tc_fence_before();
+          mbar_arrive(&bars.oR_ready);
+          if (threadIdx.x == 288) TRACE(TR_C_R, n);
+        } else {
+          mbar_arrive(&bars.oL_ready);     // first block of the unit: PV starts a fresh accumulator
+          mbar_arrive(&bars.oR_ready);
+        }
+      }
+      // ---------------- epilogue: fp32 partial o and LSE of this split
+      mbar_wait(&bars.oL_done, (n - 1) & 1);
+      mbar_wait(&bars.oR_done, (n - 1) & 1);
+      tc_fence_after();
+      const uint32_t sb = unit & 1;
+      mbar_wait(&bars.st_full[sb], (unit >> 1) & 1);
+      const float f = bars.stat[sb][r][0];
+      const float lse = bars.stat[sb][r][1];
+      mbar_arrive(&bars.st_empty[sb]);
       const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 32) {
+      for (int c = 0; c < 512; c += 64) {
+        // threads 0-15: cols [c, c+32); threads 16-31: cols [c+32, c+64)
         uint32_t ov[32];
-        tmem_ld_16x32bx2_x32<256>(tmem_O + lane_base + c, ov);
+        tmem_ld_16x32bx2_x32<32>(tmem_O + lane_base + c, ov);
         tmem_wait_ld();
         if (row_ok) {
-          float4* dst = reinterpret_cast<float4*>(p.o_part + prow * kDc + 256 * h + c);
+          float4* dst = reinterpret_cast<float4*>(p.o_part + prow * kDc + c + 32 * h);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(__uint_as_float(ov[4 * i]) * f, __uint_as_float(ov[4 * i + 1]) * f,
                                  __uint_as_float(ov[4 * i + 2]) * f, __uint_as_float(ov[4 * i + 3]) * f);
         }
       }
-      if (row_ok && h == 0) p.lse_part[prow] = (m_run * c_row + log2f(l_tot)) * 0.69314718055994531f;
+      if (row_ok && h == 0) p.lse_part[prow] = lse;
       tc_fence_before();
+      ++unit;
     }
   }
 
@@ -477,6 +578,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x + 1] = gt;
   }
 }
 
@@ -511,6 +617,8 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static unsigned long long* g_trace = nullptr;
+
 int device_num_sms() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -521,6 +629,9 @@ int device_num_sms() {
 }  // namespace snapmla
 
 using namespace snapmla;
+
+// Debug only (include/snapmla_debug.h): subsequent decodes record a CTA-0 event timeline.
+extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
 
 extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms) {
   if (batch < 0 || num_heads <= 0) return 0;
@@ -584,6 +695,20 @@ extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const
   prm.n_ht = n_ht;
   prm.max_pages = max_pages_per_seq;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
-  mla_decode_kernel<<<groups * n_ht, kThreads, kSmemBytes, st>>>(tm_kv, tm_rope, prm);
+  prm.trace = g_trace;
+  // programmatic dependent launch: the decode CTAs start (barrier init, TMEM
+  // alloc, descriptor prefetch) while the plan kernel runs; griddepcontrol.wait
+  // in the kernel orders every read of the plan / cache after it.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * n_ht);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, mla_decode_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
 }
