@@ -28,18 +28,19 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, hang_check=False, out=None):
+    lib = out or LIB
+    if not force and not hang_check and out is None and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES]]
+    extra = ["-DSNAPMLA_HANG_CHECK"] if hang_check else []
+    cmd = [NVCC, *FLAGS, *extra, "-o", lib, *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed building libsnapmla.so")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, hang_check="--hang-check" in sys.argv))

@@ -7,29 +7,46 @@
 //
 // B200 design: one persistent CTA per SM, one 64-row query-head
 // tile per CTA (UMMA M = 64), split-KV over 64-token key blocks planned on the
-// device, a 4-slot ring of 64-token KV blocks in SMEM.  Warp roles (13 warps):
-//   warp 0       TMA producer: per block 4 x 8 KB FP8 boxes + 8 KB BF16 RoPE box
+// device, a 4-slot ring of KV blocks in SMEM.  Warp roles (16 warps; the SM
+// schedulers prefer the highest eligible warp id, so latency-critical roles
+// get the high ids):
+//   warps 0-7    two accumulator warpgroups (O columns 0-255 / 256-511): the
+//                scalar Alg.1 recurrence (m, sigma_p, l, gamma; steps 4, 8-10)
+//                and O <- gamma O + T_n with O in REGISTERS (as Alg.1 keeps
+//                o^L / o^R in registers), epilogue (fp32 split partials)
+//   warp 8       TMA producer: per block 4 x 8 KB FP8 boxes + 8 KB BF16 RoPE box
 //                (SWIZZLE_128B, row coordinate from the block table) + 256 B scales
-//   warps 1, 2   QK issuers for even / odd blocks (warp 1 also owns TMEM):
-//                16 x kind::f8f6f4 (K=32) + 4 x kind::f16 (K=16) into ONE fp32
-//                accumulator S (Eq.6 makes the two domains agree)
-//   warps 3, 4   PV_L / PV_R issuers: P' (SMEM, K-major) x V (the SAME FP8 tile
-//                read MN-major: no transpose) into O_L / O_R
-//   warps 5-8    Q-quant prologue (Fused-Q-Quant), online softmax, scale fusion,
-//                block P quantization; thread = (head row, 32-token half)
-//   warps 9-12   correction O_L / O_R <- gamma O in TMEM, epilogue (fp32 partials)
-// Issue warps run converged and elect one lane per tcgen05 op.  Measured on
-// B200 (scripts/mma_bench.cu): a tcgen05.commit stalls the issuing warp's next
-// MMA until completion, so every MMA stream that commits gets its own warp and
-// the streams overlap in the tensor pipe.
-// TMEM (512 cols): O in the lower half-subpartitions (lanes 0-15 of each 32),
-// four S buffers (64 cols each) in the upper half-subpartitions (lanes 16-31).
+//   warp 9       QK issuer (owns TMEM): 16 x kind::f8f6f4 (K=32) + 4 x kind::f16
+//                (K=16) into ONE fp32 accumulator S (Eq.6 makes the domains agree)
+//   warps 10, 11 PV_L / PV_R issuers: T_n = P'_n (SMEM, K-major) x V (the SAME
+//                FP8 tile read MN-major: no transpose), a fresh TMEM tile per block
+//   warps 12-15  Q-quant prologue (Fused-Q-Quant), softmax, scale fusion, block
+//                P quantization; thread = (head row, 32-token half)
+// Why O lives in registers (measured, scripts/tmem_bench.cu): TMEM stores run at
+// ~235 B/cycle/SM, so rescaling a 64 x 512 fp32 O in TMEM every block costs
+// >= 550 cycles and serialises PV(n-1) -> rescale -> PV(n).  Reading T_n (loads
+// ~800 B/cycle) and FMA-ing into registers removes the stores and the chain.
+// Each block's softmax is computed against its OWN max (the P' codes depend only
+// on w / max_block(w)), and the accumulator warps, which see blocks in
+// strictly increasing order, carry the running max, so blocks are independent.
+// Issue warps run converged and elect one lane per tcgen05 op (measured: a
+// tcgen05.commit stalls the issuing warp's next MMA until completion, so each
+// committing MMA stream has its own warp).
+// TMEM (512 cols): T_L / T_R in the lower half-subpartitions (lanes 0-15 of each
+// 32, cols 0-255 / 256-511), four S slots (64 cols) in the upper (lanes 16-31).
 #include "snapmla_internal.h"
 
 namespace snapmla {
 
-constexpr int kThreads = 416;   // 13 warps
-constexpr int kSlots = 4;       // KV / S / P' ring depth (blocks)
+constexpr int kThreads = 512;     // 16 warps
+constexpr int kWarpAcc = 0;       // 0-3  accumulator, O cols 0-255; 4-7 cols 256-511
+constexpr int kWarpTma = 8;       // 8    TMA producer
+constexpr int kWarpQk = 9;        // 9    QK issuer, owns TMEM
+constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
+constexpr int kWarpSoftmax = 12;  // 12-15 softmax
+// register budget (setmaxnreg): 256 x 184 + 128 x 40 + 128 x 104 = 65,536
+constexpr uint32_t kRegsAcc = 184, kRegsIssue = 40, kRegsSoftmax = 104;
+constexpr int kSlots = 4;         // KV / S / P' ring depth (blocks)
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
 constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
@@ -38,7 +55,7 @@ constexpr uint32_t kOffQr = 32768;                          // [64 rows x 128 B]
 constexpr uint32_t kOffP = 40960;                           // 4 slots x 4096 B, K-major core matrices
 constexpr uint32_t kOffKv = 57344;                          // 4 slots: 4 content boxes | RoPE box | scales
 constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
-constexpr uint32_t kSmemBytes = kOffBar + 3072 + 1024;      // barriers/gamma/stats + alignment slack
+constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 // instruction descriptors (M = 64)
@@ -63,7 +80,7 @@ struct DecodeParams {
 
 // debug timeline: trace[ev * kTraceN + n] = clock64() of event ev at block n (CTA 0 only)
 constexpr int kTraceN = 256;
-enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, TR_C_R, TR_NEV };
+enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, TR_C_R, TR_S1, TR_S2, TR_S3, TR_S4, TR_S5, TR_C0, TR_C1, TR_C2, TR_NEV };
 #define TRACE(ev, n)                                                                          \
   do {                                                                                        \
     if (p.trace != nullptr && blockIdx.x == 0 && (n) < (uint32_t)kTraceN)                     \
@@ -73,15 +90,13 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
 struct Bars {
   uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
   uint64_t s_full[kSlots], s_empty[kSlots];     // QK -> softmax / softmax -> QK
-  uint64_t p_full[kSlots], p_empty[kSlots];     // P', gamma: softmax -> PV + correction / PV_L + PV_R -> softmax
-  uint64_t oL_ready, oR_ready, oL_done, oR_done;   // correction <-> PV halves
-  uint64_t q_full;                    // Q-quant prologue -> QK
-  uint64_t st_full[2], st_empty[2];   // per-unit epilogue factors softmax -> correction
+  uint64_t p_full[kSlots], p_empty[kSlots];     // P' + stats: softmax -> PV, acc / PV_L + PV_R -> softmax
+  uint64_t t_full[2], t_free[2];                // T_L/T_R: PV -> acc / acc -> PV
+  uint64_t q_full;                              // Q-quant prologue -> QK
   uint32_t tmem_base;
-  float gamma[kSlots][64];
-  float stat[2][64][2];
+  float stat[kSlots][3][64];          // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
 };
-static_assert(sizeof(Bars) <= 3072, "barrier region");
+static_assert(sizeof(Bars) <= 4096, "barrier region");
 
 // ------------------------------------------------------------------ plan (a3)
 // One CTA.  cum[b] = sum_{b'<b} ceil(L_b'/64) (exclusive scan), total T.
@@ -188,31 +203,7 @@ struct UnitIter {
 };
 
 // ------------------------------------------------------------- decode kernel
-// O <- gamma O on 16 lanes x 256 columns (threads 0-15 [c, c+32), 16-31 [c+128, c+160))
-__device__ __forceinline__ void rescale_half(uint32_t taddr, float gamma) {
-  const float2 g2 = make_float2(gamma, gamma);
-#pragma unroll
-  for (int c = 0; c < 128; c += 64) {
-    uint32_t v0[32], v1[32];
-    tmem_ld_16x32bx2_x32<128>(taddr + c, v0);
-    tmem_ld_16x32bx2_x32<128>(taddr + c + 32, v1);
-    tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      float2 a = __fmul2_rn(make_float2(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])), g2);
-      v0[i] = __float_as_uint(a.x);
-      v0[i + 1] = __float_as_uint(a.y);
-      a = __fmul2_rn(make_float2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1])), g2);
-      v1[i] = __float_as_uint(a.x);
-      v1[i + 1] = __float_as_uint(a.y);
-    }
-    tmem_st_16x32bx2_x32<128>(taddr + c, v0);
-    tmem_st_16x32bx2_x32<128>(taddr + c + 32, v1);
-  }
-  tmem_wait_st();
-}
-
-// x / s for a row-constant s: rcp + one Newton/FMA correction of the quotient
+// x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
 __device__ __forceinline__ float div_by(float x, float s, float rs) {
   const float q = x * rs;
@@ -243,26 +234,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars.p_empty[i], 2);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars.st_full[i], 128);
-      mbar_init(&bars.st_empty[i], 128);
+      mbar_init(&bars.t_full[i], 1);
+      mbar_init(&bars.t_free[i], 128);
     }
-    mbar_init(&bars.oL_ready, 128);
-    mbar_init(&bars.oR_ready, 128);
-    mbar_init(&bars.oL_done, 1);
-    mbar_init(&bars.oR_done, 1);
     mbar_init(&bars.q_full, 128);
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpTma && lane == 0) {
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_rope);
   }
-  if (warp == 1) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpQk) tmem_alloc(&bars.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-  const uint32_t tmem_O = tmem;                       // lanes 0-15 (+32k): O_L cols 0-255, O_R 256-511
+  const uint32_t tmem_T = tmem;                       // lanes 0-15 (+32k): T_L cols 0-255, T_R 256-511
   const uint32_t tmem_S = tmem + (16u << 16);         // lanes 16-31 (+32k): S slot s at cols 64 s
 
   pdl_wait();   // plan (and the appends before it) visible from here on
@@ -281,93 +268,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
   Unit u;
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
-    if (lane == 0) {
-      const uint64_t pol = l2_policy_evict_first();
-      uint32_t n = 0;
+  if (warp >= kWarpTma && warp < kWarpSoftmax) {
+    regs_dec<kRegsIssue>();
+    if (warp == kWarpTma) {
+      // ============================ TMA producer ============================
+      if (lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        uint32_t n = 0;
+        while (it.next(u)) {
+          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          for (int j = u.k0; j < u.k1; ++j, ++n) {
+            const uint32_t st = n % kSlots;
+            mbar_wait(&bars.kv_empty[st], ((n / kSlots) & 1) ^ 1, 1, n);
+            TRACE(TR_TMA, n);
+            const int row = __ldg(bt + j) * kPage;
+            const uint32_t dst = sbase + kOffKv + st * kStage;
+            mbar_arrive_expect_tx(&bars.kv_full[st], kKvTx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(dst + c * kBoxBytes, &tm_kv, &bars.kv_full[st], c * 128, row, pol);
+            tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, &bars.kv_full[st], 0, row, pol);
+            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, &bars.kv_full[st], pol);
+          }
+        }
+      }
+    } else if (warp == kWarpQk) {
+      // ================================ QK issuer ================================
+      uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+        mbar_wait(&bars.q_full, unit & 1, 2, unit);
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % kSlots;
-          mbar_wait(&bars.kv_empty[st], ((n / kSlots) & 1) ^ 1);
-          TRACE(TR_TMA, n);
-          const int row = __ldg(bt + j) * kPage;
-          const uint32_t dst = sbase + kOffKv + st * kStage;
-          mbar_arrive_expect_tx(&bars.kv_full[st], kKvTx);
+          mbar_wait(&bars.kv_full[st], (n / kSlots) & 1, 3, n);
+          mbar_wait(&bars.s_empty[st], ((n / kSlots) & 1) ^ 1, 4, n);
+          tc_fence_after();
+          if (lane == 0) TRACE(TR_QK, n);
+          const uint32_t kv = sbase + kOffKv + st * kStage;
+          const uint32_t dS = tmem_S + 64 * st;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, &bars.kv_full[st], c * 128, row, pol);
-          tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, &bars.kv_full[st], 0, row, pol);
-          bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, &bars.kv_full[st], pol);
+          for (int kk = 0; kk < 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+            mma_f8_ws(dS, make_smem_desc(sbase + kOffQc + off, 16, 1024, LAYOUT_SW128),
+                      make_smem_desc(kv + off, 16, 1024, LAYOUT_SW128), kIdescQk8, kk > 0);
+          }
+#pragma unroll
+          for (int kr = 0; kr < 4; ++kr) {
+            mma_bf16_ws(dS, make_smem_desc(sbase + kOffQr + kr * 32, 16, 1024, LAYOUT_SW128),
+                        make_smem_desc(kv + 4 * kBoxBytes + kr * 32, 16, 1024, LAYOUT_SW128), kIdescQk16, 1u);
+          }
+          mma_commit_ws(&bars.s_full[st]);
+        }
+        ++unit;
+      }
+    } else {
+      // =============================== PV_L / PV_R ===============================
+      const uint32_t half = warp - kWarpPv;
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t st = n % kSlots;
+          mbar_wait(&bars.p_full[st], (n / kSlots) & 1, 5, n);              // P'(n) in SMEM
+          if (n > 0) mbar_wait(&bars.t_free[half], (n - 1) & 1, 6, n);      // T half read by the acc warps
+          tc_fence_after();
+          if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+          const uint32_t pA = sbase + kOffP + st * 4096;
+          const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint64_t a = make_smem_desc(pA + ks * 2048, 1024, 128, LAYOUT_NONE);
+            const uint64_t b = make_smem_desc(vb + ks * 4096, kBoxBytes, 1024, LAYOUT_SW128);
+            mma_f8_ws(tmem_T + 256 * half, a, b, kIdescPv, ks);
+          }
+          mma_commit_ws(&bars.t_full[half]);
+          mma_commit_ws(&bars.p_empty[st]);
+          mma_commit_ws(&bars.kv_empty[st]);
         }
       }
     }
-  } else if (warp <= 2) {
-    // =================== QK issuers (warp 1: even blocks, warp 2: odd) ===================
-    const uint32_t parity = warp - 1;
-    uint32_t n = 0, unit = 0;
-    while (it.next(u)) {
-      mbar_wait(&bars.q_full, unit & 1);
-      for (int j = u.k0; j < u.k1; ++j, ++n) {
-        if ((n & 1) != parity) continue;
-        const uint32_t st = n % kSlots;
-        mbar_wait(&bars.kv_full[st], (n / kSlots) & 1);
-        mbar_wait(&bars.s_empty[st], ((n / kSlots) & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) TRACE(TR_QK, n);
-        const uint32_t kv = sbase + kOffKv + st * kStage;
-        const uint32_t dS = tmem_S + 64 * st;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-          mma_f8_ws(dS, make_smem_desc(sbase + kOffQc + off, 16, 1024, LAYOUT_SW128),
-                    make_smem_desc(kv + off, 16, 1024, LAYOUT_SW128), kIdescQk8, kk > 0);
-        }
-#pragma unroll
-        for (int kr = 0; kr < 4; ++kr) {
-          mma_bf16_ws(dS, make_smem_desc(sbase + kOffQr + kr * 32, 16, 1024, LAYOUT_SW128),
-                      make_smem_desc(kv + 4 * kBoxBytes + kr * 32, 16, 1024, LAYOUT_SW128), kIdescQk16, 1u);
-        }
-        mma_commit_ws(&bars.s_full[st]);
-      }
-      ++unit;
-    }
-  } else if (warp <= 4) {
-    // ========================= PV_L (warp 3) / PV_R (warp 4) =========================
-    const uint32_t half = warp - 3;
-    uint64_t* ready = half == 0 ? &bars.oL_ready : &bars.oR_ready;
-    uint64_t* done = half == 0 ? &bars.oL_done : &bars.oR_done;
-    uint32_t n = 0;
-    while (it.next(u)) {
-      const uint32_t n0 = n;
-      for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % kSlots;
-        mbar_wait(&bars.p_full[st], (n / kSlots) & 1);    // P'(n) in SMEM
-        mbar_wait(ready, n & 1);                          // O half rescaled by gamma(n)
-        tc_fence_after();
-        if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
-        const uint32_t pA = sbase + kOffP + st * 4096;
-        const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const uint64_t a = make_smem_desc(pA + ks * 2048, 1024, 128, LAYOUT_NONE);
-          const uint64_t b = make_smem_desc(vb + ks * 4096, kBoxBytes, 1024, LAYOUT_SW128);
-          mma_f8_ws(tmem_O + 256 * half, a, b, kIdescPv, (n == n0 && ks == 0) ? 0u : 1u);
-        }
-        mma_commit_ws(done);
-        mma_commit_ws(&bars.p_empty[st]);
-        mma_commit_ws(&bars.kv_empty[st]);
-      }
-    }
-  } else if (warp <= 8) {
-    // ====== softmax / scale fusion / P quantization (warps 5-8): thread = (row, token half) ======
+  } else if (warp >= kWarpSoftmax) {
+    regs_dec<kRegsSoftmax>();
+    // ======= softmax / scale fusion / P quantization: thread = (row, token half) =======
     const int k = warp & 3;                  // TMEM subpartition of this warp
     const int t = lane & 15, h = lane >> 4;  // row-in-quarter, 32-token half
     const int r = 16 * k + t;                // query-head row inside the tile
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    uint32_t n = 0, unit = 0;
+    uint32_t n = 0;
     while (it.next(u)) {
       // ---------------- Fused-Q-Quant prologue (a2): row r, content half h
       float c_row;
@@ -393,13 +380,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
         c_row = sq * p.scale_log2;
-        uint8_t* qc = smem + kOffQc;
-#pragma unroll 4
+#pragma unroll 2
         for (int gch = 0; gch < 16; ++gch) {   // 16-byte chunk of codes (re-read: L1 hit)
-          uint4 v[2];
-          v[0] = row_ok ? __ldg(qrow + 32 * h + 2 * gch) : make_uint4(0, 0, 0, 0);
-          v[1] = row_ok ? __ldg(qrow + 32 * h + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v);
+          uint4 v2[2];
+          v2[0] = row_ok ? __ldg(qrow + 32 * h + 2 * gch) : make_uint4(0, 0, 0, 0);
+          v2[1] = row_ok ? __ldg(qrow + 32 * h + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -409,9 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const int byte = 256 * h + 16 * gch;          // byte offset inside the 512-B row
           const int sub = byte >> 7, c = (byte >> 4) & 7;
-          *reinterpret_cast<uint4*>(qc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          sts_u4(sbase + kOffQc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
         }
-        uint8_t* qr = smem + kOffQr;
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
           const uint4 v = row_ok ? __ldg(qrow + 64 + 4 * h + gch) : make_uint4(0, 0, 0, 0);
@@ -425,157 +410,184 @@ __global__ void __launch_bounds__(kThreads, 1)
             w[e] = *reinterpret_cast<uint32_t*>(&o2);
           }
           const int c = 4 * h + gch;
-          *reinterpret_cast<uint4*>(qr + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
         }
         fence_proxy_async_smem();
         mbar_arrive(&bars.q_full);
       }
 
       const int L = __ldg(p.seq_lens + u.b);
-      float m_run = -INFINITY;   // running max of t = S * sigma_K (Alg.1 m)
-      float l_part = 0.f;        // this thread's partial of l = sum_j 2^{(t_j - m) c}
-      float sigma_p = 1.0f;      // Alg.1 line 1
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % kSlots;
-        mbar_wait(&bars.s_full[st], (n / kSlots) & 1);
+        mbar_wait(&bars.s_full[st], (n / kSlots) & 1, 7, n);
         tc_fence_after();
-        if (threadIdx.x == 160) TRACE(TR_SM_IN, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         float tt[32];
         tmem_ld_16x32bx2_x32<32>(tmem_S + lane_base + 64 * st, *reinterpret_cast<uint32_t(*)[32]>(tt));
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars.s_empty[st]);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
 
-        // sigma_K of my 32 tokens (from the TMA'd slot)
-        const float* sk = reinterpret_cast<const float*>(smem + kOffKv + st * kStage + 5 * kBoxBytes) + 32 * h;
-        const int nvalid = min(32, L - (j * kBc + 32 * h));
-        float mx = -INFINITY;
+        // sigma_K of my 32 tokens (from the TMA'd slot), kept in registers
+        const uint32_t sk = sbase + kOffKv + st * kStage + 5 * kBoxBytes + 128 * h;
+        float sv[32];
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-          const float4 s4 = *reinterpret_cast<const float4*>(sk + i);
-          tt[i + 0] = (i + 0 < nvalid) ? tt[i + 0] * s4.x : -INFINITY;   // Alg.1 step 3
-          tt[i + 1] = (i + 1 < nvalid) ? tt[i + 1] * s4.y : -INFINITY;
-          tt[i + 2] = (i + 2 < nvalid) ? tt[i + 2] * s4.z : -INFINITY;
-          tt[i + 3] = (i + 3 < nvalid) ? tt[i + 3] * s4.w : -INFINITY;
-          mx = fmaxf(mx, fmaxf(fmaxf(tt[i], tt[i + 1]), fmaxf(tt[i + 2], tt[i + 3])));
+          const float4 s4 = lds_f4(sk + 4 * i);
+          sv[i] = s4.x;
+          sv[i + 1] = s4.y;
+          sv[i + 2] = s4.z;
+          sv[i + 3] = s4.w;
         }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        const float m_new = fmaxf(m_run, mx);                          // step 4
-        const float mc = m_new * c_row;
-        float lsum = 0.f, mb = 0.f;
+        const int nvalid = L - (j * kBc + 32 * h);   // tokens of my half inside the sequence
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 s4 = *reinterpret_cast<const float4*>(sk + i);
-          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+        for (int i = 0; i < 32; ++i) tt[i] *= sv[i];                   // Alg.1 step 3 (descale)
+        if (nvalid < 32) {                                             // ragged tail block: mask (R19)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float pe = ex2_approx(fmaf(tt[i + e], c_row, -mc));   // step 5
-            lsum += pe;
-            tt[i + e] = pe * sv[e];                                      // step 6: p * sigma_K
-            mb = fmaxf(mb, tt[i + e]);
-          }
+          for (int i = 0; i < 32; ++i) tt[i] = i < nvalid ? tt[i] : -INFINITY;
         }
+        float mx0 = fmaxf(tt[0], tt[1]), mx1 = fmaxf(tt[2], tt[3]);
+#pragma unroll
+        for (int i = 4; i < 32; i += 4) {
+          mx0 = fmaxf(mx0, fmaxf(tt[i], tt[i + 1]));
+          mx1 = fmaxf(mx1, fmaxf(tt[i + 2], tt[i + 3]));
+        }
+        float mx = fmaxf(mx0, mx1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));          // block max of t (local m)
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S2, n);
+        const float mc = mx * c_row;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        float mb0 = 0.f, mb1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float pe = ex2_approx(fmaf(tt[i], c_row, -mc));        // step 5 (local reference)
+          ls[i & 3] += pe;
+          tt[i] = pe * sv[i];                                            // step 6: p * sigma_K
+          if (i & 1) mb1 = fmaxf(mb1, tt[i]);
+          else mb0 = fmaxf(mb0, tt[i]);
+        }
+        float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        float mb = fmaxf(mb0, mb1);
         mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
-        const float alpha = ex2_approx((m_run - m_new) * c_row);       // 0 on the first block
-        l_part = l_part * alpha + lsum;
-        // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); zero-max block -> P' = 0 (R11)
-        const float inv = mb > 0.f ? __fdiv_rn(448.0f, mb) : 0.f;
-        const float sp_new = mb > 0.f ? __fdiv_rn(mb, 448.0f) : sigma_p;
-        const float gamma = alpha * __fdiv_rn(sigma_p, sp_new);        // step 9
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
+        // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
+        // P' = 0 and is skipped by the recurrence (R11)
+        const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
         uint32_t pw[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           pw[i] = cvt4_e4m3(tt[4 * i] * inv, tt[4 * i + 1] * inv, tt[4 * i + 2] * inv, tt[4 * i + 3] * inv);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
         // P' slot free once PV_L and PV_R of block n - kSlots completed
-        mbar_wait(&bars.p_empty[st], ((n / kSlots) & 1) ^ 1);
+        mbar_wait(&bars.p_empty[st], ((n / kSlots) & 1) ^ 1, 8, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
         // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
-        uint8_t* pdst = smem + kOffP + st * 4096 + r * 16;
-        *reinterpret_cast<uint4*>(pdst + (2 * h) * 1024) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-        *reinterpret_cast<uint4*>(pdst + (2 * h + 1) * 1024) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
-        if (h == 0) bars.gamma[st][r] = gamma;
+        const uint32_t pdst = sbase + kOffP + st * 4096 + r * 16;
+        sts_u4(pdst + (2 * h) * 1024, pw[0], pw[1], pw[2], pw[3]);
+        sts_u4(pdst + (2 * h + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        if (h == 0) {
+          sts_f32(smem_u32(&bars.stat[st][0][r]), mb > 0.f ? mc : -INFINITY);
+          sts_f32(smem_u32(&bars.stat[st][1][r]), __fdiv_rn(mb, 448.0f));
+          sts_f32(smem_u32(&bars.stat[st][2][r]), lsum);
+        }
         fence_proxy_async_smem();
         mbar_arrive(&bars.p_full[st]);
-        if (threadIdx.x == 160) TRACE(TR_SM_OUT, n);
-        m_run = m_new;
-        sigma_p = sp_new;
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
-      // per-row epilogue factors (a9): o = sigma_p * O / l ; L = (m c + log2 l) ln 2
-      const float l_tot = l_part + __shfl_xor_sync(0xffffffffu, l_part, 16);
-      const uint32_t sb = unit & 1;
-      mbar_wait(&bars.st_empty[sb], ((unit >> 1) & 1) ^ 1);
-      if (h == 0) {
-        bars.stat[sb][r][0] = sigma_p / l_tot;
-        bars.stat[sb][r][1] = (m_run * c_row + log2f(l_tot)) * 0.69314718055994531f;
-      }
-      mbar_arrive(&bars.st_full[sb]);
-      ++unit;
     }
   } else {
-    // ============ correction + epilogue (warps 9-12): O <- gamma O ============
+    regs_inc<kRegsAcc>();
+    // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
+    const int half = warp >> 2;              // 0: O cols 0-255 (T_L), 1: cols 256-511 (T_R)
     const int k = warp & 3;
-    const int t = lane & 15, h = lane >> 4;
+    const int t = lane & 15, hh = lane >> 4;
     const int r = 16 * k + t;
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
-    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    uint32_t n = 0, unit = 0;
+    const uint32_t taddr = tmem_T + ((uint32_t)(32 * k) << 16) + 256 * half;
+    uint32_t n = 0;
     while (it.next(u)) {
       const uint32_t n0 = n;
+      // O holds sum_b (sig_b 2^{m_b - m_O}) P'_b V in units of sig_O 2^{m_O} (log2 units);
+      // l_run = sum_b l_b 2^{m_b - m_ref}.  This thread: row r, cols 256 half + 128 hh + [0, 128).
+      float o[128];
+      float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        if (n != n0) {
-          const uint32_t st = n % kSlots;
-          mbar_wait(&bars.p_full[st], (n / kSlots) & 1);
-          const float gamma = bars.gamma[st][r];
-          mbar_wait(&bars.oL_done, (n - 1) & 1);
-          tc_fence_after();
-          rescale_half(tmem_O + lane_base, gamma);
-          tc_fence_before();
-          mbar_arrive(&bars.oL_ready);
-          if (threadIdx.x == 288) TRACE(TR_C_L, n);
-          mbar_wait(&bars.oR_done, (n - 1) & 1);
-          tc_fence_after();
-          rescale_half(tmem_O + lane_base + 256, gamma);
-          tc_fence_before();
-          mbar_arrive(&bars.oR_ready);
-          if (threadIdx.x == 288) TRACE(TR_C_R, n);
-        } else {
-          mbar_arrive(&bars.oL_ready);     // first block of the unit: PV starts a fresh accumulator
-          mbar_arrive(&bars.oR_ready);
+        const uint32_t st = n % kSlots;
+        mbar_wait(&bars.p_full[st], (n / kSlots) & 1, 9, n);
+        if (threadIdx.x == 0) TRACE(TR_C0, n);
+        const float mb = lds_f32(smem_u32(&bars.stat[st][0][r]));
+        const float sb = lds_f32(smem_u32(&bars.stat[st][1][r]));
+        const float lb = lds_f32(smem_u32(&bars.stat[st][2][r]));
+        const float m_new = fmaxf(m_ref, mb);                          // step 4 (running max)
+        // a block whose contributions are < 2^-64 of the running total is dropped
+        // (Alg.1 loses it to fp32 underflow of exp(s - m)); so is a zero-max block
+        const bool first = n == n0;
+        const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
+        float gamma = 1.f;
+        if (first) {
+          m_O = mb;
+          sig_O = sb;
+          l_run = lb;
+          m_ref = mb;
+        } else if (!skip) {
+          gamma = ex2_approx(m_O - mb) * __fdiv_rn(sig_O, sb);         // steps 9-10
+          l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
+          m_ref = m_new;
+          m_O = mb;
+          sig_O = sb;
         }
-      }
-      // ---------------- epilogue: fp32 partial o and LSE of this split
-      mbar_wait(&bars.oL_done, (n - 1) & 1);
-      mbar_wait(&bars.oR_done, (n - 1) & 1);
-      tc_fence_after();
-      const uint32_t sb = unit & 1;
-      mbar_wait(&bars.st_full[sb], (unit >> 1) & 1);
-      const float f = bars.stat[sb][r][0];
-      const float lse = bars.stat[sb][r][1];
-      mbar_arrive(&bars.st_empty[sb]);
-      const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
-#pragma unroll 1
-      for (int c = 0; c < 512; c += 64) {
-        // threads 0-15: cols [c, c+32); threads 16-31: cols [c+32, c+64)
-        uint32_t ov[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_O + lane_base + c, ov);
-        tmem_wait_ld();
-        if (row_ok) {
-          float4* dst = reinterpret_cast<float4*>(p.o_part + prow * kDc + c + 32 * h);
+        mbar_wait(&bars.t_full[half], n & 1, 10, n);                   // T(n) = P'(n) V complete
+        tc_fence_after();
+        if (threadIdx.x == 0) TRACE(TR_C1, n);
+        const float2 g2 = make_float2(gamma, gamma);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(ov[4 * i]) * f, __uint_as_float(ov[4 * i + 1]) * f,
-                                 __uint_as_float(ov[4 * i + 2]) * f, __uint_as_float(ov[4 * i + 3]) * f);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t tv[32];
+          tmem_ld_16x32bx2_x32<128>(taddr + 32 * c, tv);
+          tmem_wait_ld();
+          if (c == 3) {
+            tc_fence_before();
+            mbar_arrive(&bars.t_free[half]);                           // PV(n+1) may overwrite T
+          }
+          if (first) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[32 * c + i] = __uint_as_float(tv[i]);
+          } else if (!skip) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float2 a = __ffma2_rn(make_float2(o[32 * c + i], o[32 * c + i + 1]), g2,
+                                          make_float2(__uint_as_float(tv[i]), __uint_as_float(tv[i + 1])));
+              o[32 * c + i] = a.x;
+              o[32 * c + i + 1] = a.y;
+            }
+          }
         }
+        if (threadIdx.x == 0) TRACE(TR_C_L, n);
       }
-      if (row_ok && h == 0) p.lse_part[prow] = lse;
-      tc_fence_before();
-      ++unit;
+      // ---------------- epilogue (a9): o = sig_O 2^{m_O - m_ref} O / l ; L = (m_ref + log2 l) ln 2
+      const float f = sig_O * ex2_approx(m_O - m_ref) / l_run;
+      const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
+      if (row_ok) {
+        float* dst = p.o_part + prow * kDc + 256 * half + 128 * hh;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          // chunk c of this thread = TMEM cols [32c, 32c+32) (+128 for threads 16-31)
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + 32 * c + i) =
+                make_float4(o[32 * c + i] * f, o[32 * c + i + 1] * f, o[32 * c + i + 2] * f, o[32 * c + i + 3] * f);
+        }
+        if (half == 0 && hh == 0) p.lse_part[prow] = (m_ref + log2f(l_run)) * 0.69314718055994531f;
+      }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kWarpQk) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #define DEVI __device__ __forceinline__
 
@@ -37,10 +38,42 @@ DEVI bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SNAPMLA_HANG_CHECK
+// debug build: report and trap if a barrier wait exceeds ~2^31 cycles
+DEVI void mbar_wait(uint64_t* bar, uint32_t parity, int tag = -1, int idx = -1) {
+  const uint32_t a = smem_u32(bar);
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << 31)) {
+      printf("HANG block %d thread %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x, tag, idx, parity);
+      __trap();
+    }
+  }
+}
+#else
+DEVI void mbar_wait(uint64_t* bar, uint32_t parity, int = -1, int = -1) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait(a, parity)) {
   }
+}
+#endif
+
+// ------------------------------------------------------- shared-space access
+DEVI float4 lds_f4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
+DEVI float lds_f32(uint32_t saddr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+  return v;
+}
+DEVI void sts_u4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+DEVI void sts_f32(uint32_t saddr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
 }
 
 // ------------------------------------------------------------------ fences

@@ -20,7 +20,8 @@ for s in range(0, n_tok, 1 << 18):
     cache.append(c, r, bt[req, pos // 64].view(-1, 1).contiguous(), (pos % 64 + 1).to(torch.int32))
 q = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
 sl = torch.full((B,), L, dtype=torch.int32, device=dev)
-tr = torch.zeros(8 * 256 + 2 * 1024, dtype=torch.int64, device=dev)
+NEV = 16
+tr = torch.zeros(NEV * 256 + 2 * 1024, dtype=torch.int64, device=dev)
 lib = ops.lib()
 lib.mla_debug_set_trace.argtypes = [ctypes.c_void_p]
 for i in range(3):
@@ -30,26 +31,26 @@ for i in range(3):
 torch.cuda.synchronize()
 lib.mla_debug_set_trace(None)
 allt = tr.cpu().numpy().astype(np.int64)
-t = allt[:2048].reshape(8, 256)
-ct = allt[2048:].reshape(-1, 2)
+t = allt[:NEV * 256].reshape(NEV, 256)
+ct = allt[NEV * 256:].reshape(-1, 2)
 ct = ct[ct[:, 0] > 0]
 t0g = ct[:, 0].min()
 dur = (ct[:, 1] - ct[:, 0]) / 1e3
 print('CTAs', len(ct), 'start spread us', (ct[:, 0].max() - t0g) / 1e3, 'duration us min/median/max', dur.min(), np.median(dur), dur.max(), 'kernel span us', (ct[:, 1].max() - t0g) / 1e3)
 print('durations sorted (us):', np.round(np.sort(dur)[::10], 1))
-names = ["TMA", "QK", "PV_L", "PV_R", "SM_in", "SM_out", "C_L", "C_R"]
+names = ["TMA", "QK", "PV_L", "PV_R", "SM_in", "SM_out", "C_L", "C_R", "S1", "S2", "S3", "S4", "S5", "C0", "C1", "C2"]
 valid = t[1] > 0
 nv = int(valid.sum())
 t0 = t[0][0]
 rel = np.where(t > 0, t - t0, 0)
 print("blocks traced:", nv)
-print("  n " + " ".join(f"{nm:>8}" for nm in names))
+print("  n " + " ".join(f"{nm:>7}" for nm in names))
 for n in list(range(0, 12)) + list(range(100, 108)):
     if n < nv:
-        print(f"{n:3d} " + " ".join(f"{rel[e][n]:8d}" for e in range(8)))
+        print(f"{n:3d} " + " ".join(f"{rel[e][n]:7d}" for e in range(NEV)))
 d = np.diff(t[1][:nv])
 print("QK issue period: median", np.median(d[10:]), "mean", d[10:].mean())
-for e in range(8):
+for e in range(NEV):
     dd = np.diff(t[e][20:nv])
     print(f"{names[e]:>7} period median {np.median(dd):.0f}")
 print("SM_out - SM_in median", np.median((t[5] - t[4])[20:nv]))
@@ -58,3 +59,8 @@ print("PV_L - C_L median", np.median((t[2] - t[6])[20:nv]))
 print("C_R - C_L median", np.median((t[7] - t[6])[20:nv]))
 print("SM_in - QK median", np.median((t[4] - t[1])[20:nv]))
 print("QK(n) - TMA(n) median", np.median((t[1] - t[0])[20:nv]))
+
+def med(a, b):
+    return np.median((t[b] - t[a])[20:nv])
+print("softmax: S1-SM_in", med(4, 8), "S2-S1", med(8, 9), "S3-S2", med(9, 10), "S4-S3", med(10, 11), "S5-S4", med(11, 12), "SM_out-S5", med(12, 5))
+print("corr: C0-prevC_R", np.median((t[13][21:nv] - t[7][20:nv-1])), "C1-C0", med(13, 14), "C_L-C1", med(14, 6), "C2-C_L", med(6, 15), "C_R-C2", med(15, 7))
