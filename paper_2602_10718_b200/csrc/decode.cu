@@ -44,8 +44,8 @@ constexpr int kWarpTma = 8;       // 8    TMA producer
 constexpr int kWarpQk = 9;        // 9    QK issuer, owns TMEM
 constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
 constexpr int kWarpSoftmax = 12;  // 12-15 softmax
-// register budget (setmaxnreg): 256 x 184 + 128 x 40 + 128 x 104 = 65,536
-constexpr uint32_t kRegsAcc = 184, kRegsIssue = 40, kRegsSoftmax = 104;
+// register budget (setmaxnreg): 256 x 192 + 128 x 40 + 128 x 88 = 65,536
+constexpr uint32_t kRegsAcc = 192, kRegsIssue = 40, kRegsSoftmax = 88;
 constexpr int kSlots = 4;         // KV / S / P' ring depth (blocks)
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
@@ -543,25 +543,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (threadIdx.x == 0) TRACE(TR_C1, n);
         const float2 g2 = make_float2(gamma, gamma);
+        // software-pipelined T reads (8 chunks of 16 columns): chunk c+1 is in
+        // flight while chunk c is FMA'd
+        uint32_t tv[2][16];
+        tmem_ld_16x32bx2_x16<128>(taddr, tv[0]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t tv[32];
-          tmem_ld_16x32bx2_x32<128>(taddr + 32 * c, tv);
+        for (int c = 0; c < 8; ++c) {
           tmem_wait_ld();
-          if (c == 3) {
+          if (c < 7) tmem_ld_16x32bx2_x16<128>(taddr + 16 * (c + 1), tv[(c + 1) & 1]);
+          else {
             tc_fence_before();
             mbar_arrive(&bars.t_free[half]);                           // PV(n+1) may overwrite T
           }
+          const uint32_t* cur = tv[c & 1];
           if (first) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[32 * c + i] = __uint_as_float(tv[i]);
+            for (int i = 0; i < 16; ++i) o[16 * c + i] = __uint_as_float(cur[i]);
           } else if (!skip) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float2 a = __ffma2_rn(make_float2(o[32 * c + i], o[32 * c + i + 1]), g2,
-                                          make_float2(__uint_as_float(tv[i]), __uint_as_float(tv[i + 1])));
-              o[32 * c + i] = a.x;
-              o[32 * c + i + 1] = a.y;
+            for (int i = 0; i < 16; i += 2) {
+              const float2 a = __ffma2_rn(make_float2(o[16 * c + i], o[16 * c + i + 1]), g2,
+                                          make_float2(__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])));
+              o[16 * c + i] = a.x;
+              o[16 * c + i + 1] = a.y;
             }
           }
         }
