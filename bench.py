@@ -134,13 +134,15 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
+    from paper_2602_10718_b200 import dist as D
     from paper_2602_10718_b200 import ops, synth
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     w = workload(args)
     B, H, L = w["batch"], w["heads"], w["context"]
-    heads_local = H // world if args.mode == "tp" else H
+    head0, head1 = D.tp_range(H, world, rank) if args.mode == "tp" else (0, H)
+    heads_local = head1 - head0
     scale = synth.DEFAULT_SOFTMAX_SCALE
 
     gen = torch.Generator(device=dev)
@@ -163,8 +165,7 @@ def run_ours(args, rank, world, local_rank):
         c, r = synth.torch_latent(idx.numel(), gen, dev)
         cache.append(c, r, bt_v, sl_v)
     q_all = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
-    head0 = rank * heads_local if args.mode == "tp" else 0
-    q = q_all[:, head0:head0 + heads_local].contiguous()
+    q = q_all[:, head0:head1].contiguous()
     new_c, new_r = synth.torch_latent(B, gen, dev)
     seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
     ws = torch.empty(ops.mla_decode_workspace_bytes(B, heads_local), dtype=torch.uint8, device=dev)
@@ -188,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
             ev_d1[i].record(stream)
         ops.mla_combine(ws, B, heads_local, out, lse)
         if gathered is not None:
-            dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
+            D.tp_gather_heads(out, gathered=gathered)
 
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -239,10 +240,9 @@ def run_ours(args, rank, world, local_rank):
         cache.append(c_d, r_d, block_table, seq_lens)
         ops.mla_decode_fp8(q_d, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
         ops.mla_combine(ws, B, heads_local, out, lse)
-        res = out
         if gathered is not None:
-            dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
-        out_h.copy_(res, non_blocking=True)
+            D.tp_gather_heads(out, gathered=gathered)
+        out_h.copy_(out, non_blocking=True)
         lse_h.copy_(lse, non_blocking=True)
 
     for _ in range(3):
