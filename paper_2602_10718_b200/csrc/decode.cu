@@ -431,18 +431,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         // sigma_K of my 32 tokens (from the TMA'd slot), kept in registers
         const uint32_t sk = sbase + kOffKv + st * kStage + 5 * kBoxBytes + 128 * h;
-        float sv[32];
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 s4 = lds_f4(sk + 4 * i);
-          sv[i] = s4.x;
-          sv[i + 1] = s4.y;
-          sv[i + 2] = s4.z;
-          sv[i + 3] = s4.w;
-        }
         const int nvalid = L - (j * kBc + 32 * h);   // tokens of my half inside the sequence
 #pragma unroll
-        for (int i = 0; i < 32; ++i) tt[i] *= sv[i];                   // Alg.1 step 3 (descale)
+        for (int i = 0; i < 32; i += 4) {                              // Alg.1 step 3 (descale)
+          const float4 s4 = lds_f4(sk + 4 * i);
+          const float2 a = __fmul2_rn(make_float2(tt[i], tt[i + 1]), make_float2(s4.x, s4.y));
+          const float2 b = __fmul2_rn(make_float2(tt[i + 2], tt[i + 3]), make_float2(s4.z, s4.w));
+          tt[i] = a.x;
+          tt[i + 1] = a.y;
+          tt[i + 2] = b.x;
+          tt[i + 3] = b.y;
+        }
         if (nvalid < 32) {                                             // ragged tail block: mask (R19)
 #pragma unroll
           for (int i = 0; i < 32; ++i) tt[i] = i < nvalid ? tt[i] : -INFINITY;
@@ -460,12 +459,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
         float mb0 = 0.f, mb1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float pe = ex2_approx(fmaf(tt[i], c_row, -mc));        // step 5 (local reference)
-          ls[i & 3] += pe;
-          tt[i] = pe * sv[i];                                            // step 6: p * sigma_K
-          if (i & 1) mb1 = fmaxf(mb1, tt[i]);
-          else mb0 = fmaxf(mb0, tt[i]);
+        for (int i = 0; i < 32; i += 4) {
+          const float4 s4 = lds_f4(sk + 4 * i);                        // sigma_K (re-read, LDS broadcast)
+          const float2 e0 = __ffma2_rn(make_float2(tt[i], tt[i + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 e1 = __ffma2_rn(make_float2(tt[i + 2], tt[i + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));   // step 5 (block reference)
+          const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
+          const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));           // step 6: p * sigma_K
+          const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
+          ls[0] += p0.x;
+          ls[1] += p0.y;
+          ls[2] += p1.x;
+          ls[3] += p1.y;
+          tt[i] = w0.x;
+          tt[i + 1] = w0.y;
+          tt[i + 2] = w1.x;
+          tt[i + 3] = w1.y;
+          mb0 = fmaxf(mb0, fmaxf(w0.x, w0.y));
+          mb1 = fmaxf(mb1, fmaxf(w1.x, w1.y));
         }
         float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
         float mb = fmaxf(mb0, mb1);
