@@ -28,11 +28,12 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, hang_check=False, out=None):
+def build(force=False, verbose=False, hang_check=False, out=None, defines=()):
+    """Compile libsnapmla.so (or `out`); `defines` are extra -D macros for experiment variants."""
     lib = out or LIB
-    if not force and not hang_check and out is None and not _stale():
+    if not force and not hang_check and out is None and not defines and not _stale():
         return LIB
-    extra = ["-DSNAPMLA_HANG_CHECK"] if hang_check else []
+    extra = (["-DSNAPMLA_HANG_CHECK"] if hang_check else []) + [f"-D{d}" for d in defines]
     cmd = [NVCC, *FLAGS, *extra, "-o", lib, *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:

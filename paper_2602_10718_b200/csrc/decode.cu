@@ -5,11 +5,11 @@
 // quantization + implicit dequantization, Algorithm 1
 // with Appendix C's strictly monotonic accumulation order.
 //
-// B200 design (DESIGN.md §5): one persistent CTA per SM, one 64-row query-head
+// B200 design (DESIGN.md §7.3): one persistent CTA per SM, one 64-row query-head
 // tile per CTA (UMMA M = 64), split-KV over 64-token key blocks planned on the
 // device, a 4-slot ring of KV blocks in SMEM.  Warp roles (16 warps; the SM
-// schedulers prefer the highest eligible warp id, so latency-critical roles
-// get the high ids):
+// schedulers prefer the highest eligible warp id, so latency-critical roles get
+// the high ids):
 //   warps 0-7    two accumulator warpgroups (O columns 0-255 / 256-511): the
 //                scalar Alg.1 recurrence (m, sigma_p, l, gamma; steps 4, 8-10)
 //                and O <- gamma O + T_n with O in REGISTERS (as Alg.1 keeps
@@ -18,35 +18,39 @@
 //                (SWIZZLE_128B, row coordinate from the block table) + 256 B scales
 //   warp 9       QK issuer (owns TMEM): 16 x kind::f8f6f4 (K=32) + 4 x kind::f16
 //                (K=16) into ONE fp32 accumulator S (Eq.6 makes the domains agree)
-//   warps 10, 11 PV_L / PV_R issuers: T_n = P'_n (SMEM, K-major) x V (the SAME
-//                FP8 tile read MN-major: no transpose), a fresh TMEM tile per block
+//   warps 10, 11 PV_L / PV_R issuers: T = P'_n (SMEM, K-major) x V (the SAME
+//                FP8 tile read MN-major: no transpose) into a 3-slot TMEM ring
 //   warps 12-15  Q-quant prologue (Fused-Q-Quant), softmax, scale fusion, block
 //                P quantization; thread = (head row, 32-token half)
 // Why O lives in registers (measured, scripts/tmem_bench.cu): TMEM stores run at
 // ~235 B/cycle/SM, so rescaling a 64 x 512 fp32 O in TMEM every block costs
-// >= 550 cycles and serialises PV(n-1) -> rescale -> PV(n).  Reading T_n (loads
-// ~800 B/cycle) and FMA-ing into registers removes the stores and the chain.
+// >= 550 cycles and serialises PV(n-1) -> rescale -> PV(n).
+// Issue economy (measured, scripts/acc_bench.cu + ncu source counters): the
+// accumulate step is issue-bound when it shares an SMSP with busy higher-priority
+// warps, so the per-block instruction count is kept minimal: one elect per MMA
+// block (single asm), u32 shared-window barrier addresses, packed f32x2 math,
+// a branch-free first block (gamma = 0 on a zeroed O), E4M3 packing via F2FP
+// merge, and the debug timeline compiled out of production builds.
 // Each block's softmax is computed against its OWN max (the P' codes depend only
-// on w / max_block(w)), and the accumulator warps, which see blocks in
-// strictly increasing order, carry the running max, so blocks are independent.
-// Issue warps run converged and elect one lane per tcgen05 op (measured: a
-// tcgen05.commit stalls the issuing warp's next MMA until completion, so each
-// committing MMA stream has its own warp).
-// TMEM (512 cols): T_L / T_R in the lower half-subpartitions (lanes 0-15 of each
-// 32, cols 0-255 / 256-511), four S slots (64 cols) in the upper (lanes 16-31).
+// on w / max_block(w)); the accumulator warps carry the running max.
+// TMEM (512 cols): lanes 0-15 of each 32-lane subpartition hold T slots 0 / 1
+// (cols 0-255 / 256-511); lanes 16-31 hold four S slots (cols 64 s) and T slot 2
+// (cols 256-511).  PV half h = 2n + (0: L, 1: R) goes to T slot h % 3, so PV(n+1)
+// overlaps the accumulation of block n.
 #include "snapmla_internal.h"
 
 namespace snapmla {
 
 constexpr int kThreads = 512;     // 16 warps
-constexpr int kWarpAcc = 0;       // 0-3  accumulator, O cols 0-255; 4-7 cols 256-511
-constexpr int kWarpTma = 8;       // 8    TMA producer
-constexpr int kWarpQk = 9;        // 9    QK issuer, owns TMEM
+constexpr int kWarpAcc = 0;       // 0-3 accumulators, O cols 0-255; 4-7 cols 256-511
+constexpr int kWarpTma = 8;       // 8     TMA producer
+constexpr int kWarpQk = 9;        // 9     QK issuer, owns TMEM
 constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
 constexpr int kWarpSoftmax = 12;  // 12-15 softmax
-// register budget (setmaxnreg): 256 x 192 + 128 x 40 + 128 x 88 = 65,536
+// register budget (setmaxnreg): 256 x 192 + 128 x 40 + 128 x 88 = 65,536 = 512 x 128 (launch)
 constexpr uint32_t kRegsAcc = 192, kRegsIssue = 40, kRegsSoftmax = 88;
 constexpr int kSlots = 4;         // KV / S / P' ring depth (blocks)
+constexpr int kTSlots = 3;        // TMEM ring of 64 x 256 PV half tiles
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
 constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
@@ -75,28 +79,35 @@ struct DecodeParams {
   float* o_part;
   int batch, num_heads, n_ht, max_pages;
   float scale_log2;   // softmax_scale * log2(e)
-  unsigned long long* trace;   // debug timeline (CTA 0), nullptr in production
+  unsigned long long* trace;   // debug timeline (CTA 0), only in SNAPMLA_TRACE builds
 };
 
-// debug timeline: trace[ev * kTraceN + n] = clock64() of event ev at block n (CTA 0 only)
+// debug timeline (SNAPMLA_TRACE builds only): trace[ev * kTraceN + n] = clock64() of event ev at block n (CTA 0)
 constexpr int kTraceN = 256;
 enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, TR_C_R, TR_S1, TR_S2, TR_S3, TR_S4, TR_S5, TR_C0, TR_C1, TR_C2, TR_NEV };
+#ifdef SNAPMLA_TRACE
 #define TRACE(ev, n)                                                                          \
   do {                                                                                        \
     if (p.trace != nullptr && blockIdx.x == 0 && (n) < (uint32_t)kTraceN)                     \
       p.trace[(ev) * kTraceN + (n)] = clock64();                                              \
   } while (0)
+#else
+#define TRACE(ev, n) \
+  do {               \
+  } while (0)
+#endif
 
 struct Bars {
   uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
-  uint64_t s_full[kSlots], s_empty[kSlots];     // QK -> softmax / softmax -> QK
-  uint64_t p_full[kSlots], p_empty[kSlots];     // P' + stats: softmax -> PV, acc / PV_L + PV_R -> softmax
-  uint64_t t_full[2], t_free[2];                // T_L/T_R: PV -> acc / acc -> PV
-  uint64_t q_full;                              // Q-quant prologue -> QK
+  uint64_t s_full[kSlots], s_empty[kSlots];     // QK -> softmax WG / softmax WG -> QK
+  uint64_t p_full[kSlots], p_empty[kSlots];     // P' + stats: softmax WG -> PV, WGs / PV_L + PV_R -> softmax
+  uint64_t t_full[kTSlots], t_free[kTSlots];    // T ring: PV -> WG / WG -> PV
+  uint64_t q_full, q_free;                      // Q-quant prologue -> QK / QK of a unit done -> prologue
   uint32_t tmem_base;
   float stat[kSlots][3][64];          // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
 };
 static_assert(sizeof(Bars) <= 4096, "barrier region");
+#define BAR(field) (bar0 + (uint32_t)offsetof(Bars, field))
 
 // ------------------------------------------------------------------ plan (a3)
 // One CTA.  cum[b] = sum_{b'<b} ceil(L_b'/64) (exclusive scan), total T.
@@ -202,6 +213,7 @@ struct UnitIter {
   }
 };
 
+
 // ------------------------------------------------------------- decode kernel
 // x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
@@ -210,46 +222,89 @@ __device__ __forceinline__ float div_by(float x, float s, float rs) {
   return fmaf(fmaf(-q, s, x), rs, q);
 }
 
-__device__ __forceinline__ uint32_t cvt4_e4m3(float a, float b, float c, float d) {
-  return (uint32_t)cvt_e4m3x2(a, b) | ((uint32_t)cvt_e4m3x2(c, d) << 16);
+// One QK block into S (TMEM): 16 x kind::f8f6f4 (K = 32) over the 512 content dims,
+// then 4 x kind::f16 (K = 16) over the 64 RoPE dims, accumulating into the same S;
+// commit to `bar`.  One elect for the whole block.  Descriptor start addresses
+// advance in 16-byte units: content step kk at byte (kk / 4) * 8192 + (kk % 4) * 32.
+#define SNAPMLA_QK8(ao, acc)                                                                   \
+  "add.s64 a, %1, " #ao ";\n\tadd.s64 b, %2, " #ao ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, " acc ";\n\t"
+#define SNAPMLA_QK16(ao)                                                                       \
+  "add.s64 a, %4, " #ao ";\n\tadd.s64 b, %5, " #ao ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, pt;\n\t"
+__device__ __forceinline__ void qk_issue(uint32_t dS, uint64_t dQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
+                                         uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      SNAPMLA_QK8(0, "pf") SNAPMLA_QK8(2, "pt") SNAPMLA_QK8(4, "pt") SNAPMLA_QK8(6, "pt")
+      SNAPMLA_QK8(512, "pt") SNAPMLA_QK8(514, "pt") SNAPMLA_QK8(516, "pt") SNAPMLA_QK8(518, "pt")
+      SNAPMLA_QK8(1024, "pt") SNAPMLA_QK8(1026, "pt") SNAPMLA_QK8(1028, "pt") SNAPMLA_QK8(1030, "pt")
+      SNAPMLA_QK8(1536, "pt") SNAPMLA_QK8(1538, "pt") SNAPMLA_QK8(1540, "pt") SNAPMLA_QK8(1542, "pt")
+      SNAPMLA_QK16(0) SNAPMLA_QK16(2) SNAPMLA_QK16(4) SNAPMLA_QK16(6)
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}"
+      ::"r"(dS), "l"(dQ), "l"(dK), "r"(kIdescQk8), "l"(dQr), "l"(dKr), "r"(kIdescQk16), "r"(bar)
+      : "memory");
+}
+
+// One PV half: T = P' (64 x 64 tokens, K-major) x V (64 tokens x 256 dims, MN-major),
+// 2 x kind::f8f6f4 (K = 32); commit to t_full, p_empty and kv_empty.
+__device__ __forceinline__ void pv_issue(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t, uint32_t bar_p,
+                                         uint32_t bar_kv) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPv), "r"(bar_t), "r"(bar_p), "r"(bar_kv)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t t_slot_addr(uint32_t tmem, uint32_t s) {
+  return tmem + (s == 2 ? (16u << 16) + 256u : 256u * s);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
                       const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  Bars& bars = *reinterpret_cast<Bars*>(smem + kOffBar);
-  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = sbase + kOffBar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- setup overlaps the plan kernel (programmatic dependent launch)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(&bars.kv_full[i], 1);
-      mbar_init(&bars.kv_empty[i], 2);
-      mbar_init(&bars.s_full[i], 1);
-      mbar_init(&bars.s_empty[i], 128);
-      mbar_init(&bars.p_full[i], 128);
-      mbar_init(&bars.p_empty[i], 2);
+      mbar_init(BAR(kv_full) + 8 * i, 1);
+      mbar_init(BAR(kv_empty) + 8 * i, 2);
+      mbar_init(BAR(s_full) + 8 * i, 1);
+      mbar_init(BAR(s_empty) + 8 * i, 4);
+      mbar_init(BAR(p_full) + 8 * i, 4);
+      mbar_init(BAR(p_empty) + 8 * i, 2);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars.t_full[i], 1);
-      mbar_init(&bars.t_free[i], 128);
+    for (int i = 0; i < kTSlots; ++i) {
+      mbar_init(BAR(t_full) + 8 * i, 1);
+      mbar_init(BAR(t_free) + 8 * i, 4);
     }
-    mbar_init(&bars.q_full, 128);
+    mbar_init(BAR(q_full), 4);
+    mbar_init(BAR(q_free), 1);
     fence_barrier_init();
   }
   if (warp == kWarpTma && lane == 0) {
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_rope);
   }
-  if (warp == kWarpQk) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpQk) tmem_alloc(BAR(tmem_base), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = bars.tmem_base;
-  const uint32_t tmem_T = tmem;                       // lanes 0-15 (+32k): T_L cols 0-255, T_R 256-511
+  const uint32_t tmem = lds_u32(BAR(tmem_base));
   const uint32_t tmem_S = tmem + (16u << 16);         // lanes 16-31 (+32k): S slot s at cols 64 s
 
   pdl_wait();   // plan (and the appends before it) visible from here on
@@ -259,11 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lo = g * per;
   const bool has_work = g < groups && lo < total;
   const int hi = min(total, lo + per);
+#ifdef SNAPMLA_TRACE
   if (p.trace != nullptr && threadIdx.x == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
     p.trace[TR_NEV * kTraceN + 2 * blockIdx.x] = gt;
   }
+#endif
 
   UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
   Unit u;
@@ -279,45 +336,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
           for (int j = u.k0; j < u.k1; ++j, ++n) {
             const uint32_t st = n % kSlots;
-            mbar_wait(&bars.kv_empty[st], ((n / kSlots) & 1) ^ 1, 1, n);
+            mbar_wait_backoff(BAR(kv_empty) + 8 * st, ((n / kSlots) & 1) ^ 1);
             TRACE(TR_TMA, n);
             const int row = __ldg(bt + j) * kPage;
             const uint32_t dst = sbase + kOffKv + st * kStage;
-            mbar_arrive_expect_tx(&bars.kv_full[st], kKvTx);
+            const uint32_t full = BAR(kv_full) + 8 * st;
+            mbar_arrive_expect_tx(full, kKvTx);
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              tma_load_2d(dst + c * kBoxBytes, &tm_kv, &bars.kv_full[st], c * 128, row, pol);
-            tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, &bars.kv_full[st], 0, row, pol);
-            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, &bars.kv_full[st], pol);
+            for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, full, c * 128, row, pol);
+            tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, full, 0, row, pol);
+            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, full, pol);
           }
         }
       }
     } else if (warp == kWarpQk) {
       // ================================ QK issuer ================================
+      const uint64_t dQ = make_smem_desc(sbase + kOffQc, 16, 1024, LAYOUT_SW128);
+      const uint64_t dQr = make_smem_desc(sbase + kOffQr, 16, 1024, LAYOUT_SW128);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        mbar_wait(&bars.q_full, unit & 1, 2, unit);
+        mbar_wait(BAR(q_full), unit & 1, 2, unit);
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % kSlots;
-          mbar_wait(&bars.kv_full[st], (n / kSlots) & 1, 3, n);
-          mbar_wait(&bars.s_empty[st], ((n / kSlots) & 1) ^ 1, 4, n);
+          mbar_wait(BAR(kv_full) + 8 * st, (n / kSlots) & 1, 3, n);
+          mbar_wait(BAR(s_empty) + 8 * st, ((n / kSlots) & 1) ^ 1, 4, n);
           tc_fence_after();
           if (lane == 0) TRACE(TR_QK, n);
           const uint32_t kv = sbase + kOffKv + st * kStage;
-          const uint32_t dS = tmem_S + 64 * st;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-            mma_f8_ws(dS, make_smem_desc(sbase + kOffQc + off, 16, 1024, LAYOUT_SW128),
-                      make_smem_desc(kv + off, 16, 1024, LAYOUT_SW128), kIdescQk8, kk > 0);
-          }
-#pragma unroll
-          for (int kr = 0; kr < 4; ++kr) {
-            mma_bf16_ws(dS, make_smem_desc(sbase + kOffQr + kr * 32, 16, 1024, LAYOUT_SW128),
-                        make_smem_desc(kv + 4 * kBoxBytes + kr * 32, 16, 1024, LAYOUT_SW128), kIdescQk16, 1u);
-          }
-          mma_commit_ws(&bars.s_full[st]);
+          qk_issue(tmem_S + 64 * st, dQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                   make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * st);
         }
+        mma_commit_ws(BAR(q_free));   // Q SMEM reusable once this unit's QK MMAs completed
         ++unit;
       }
     } else {
@@ -327,47 +376,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % kSlots;
-          mbar_wait(&bars.p_full[st], (n / kSlots) & 1, 5, n);              // P'(n) in SMEM
-          if (n > 0) mbar_wait(&bars.t_free[half], (n - 1) & 1, 6, n);      // T half read by the acc warps
+          const uint32_t h = 2 * n + half, ts = h % kTSlots;
+          mbar_wait(BAR(p_full) + 8 * st, (n / kSlots) & 1, 5, n);                   // P'(n) in SMEM
+          if (h >= kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / kTSlots - 1) & 1, 6, n);   // slot read
           tc_fence_after();
           if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
           const uint32_t pA = sbase + kOffP + st * 4096;
           const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t a = make_smem_desc(pA + ks * 2048, 1024, 128, LAYOUT_NONE);
-            const uint64_t b = make_smem_desc(vb + ks * 4096, kBoxBytes, 1024, LAYOUT_SW128);
-            mma_f8_ws(tmem_T + 256 * half, a, b, kIdescPv, ks);
-          }
-          mma_commit_ws(&bars.t_full[half]);
-          mma_commit_ws(&bars.p_empty[st]);
-          mma_commit_ws(&bars.kv_empty[st]);
+          pv_issue(t_slot_addr(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                   make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
+                   BAR(p_empty) + 8 * st, BAR(kv_empty) + 8 * st);
         }
       }
     }
   } else if (warp >= kWarpSoftmax) {
     regs_dec<kRegsSoftmax>();
-    // ======= softmax / scale fusion / P quantization: thread = (row, token half) =======
+    // ======= softmax / scale fusion / P quantization: thread = (row, 32-token half) =======
     const int k = warp & 3;                  // TMEM subpartition of this warp
-    const int t = lane & 15, h = lane >> 4;  // row-in-quarter, 32-token half
+    const int t = lane & 15, hh = lane >> 4; // row-in-quarter, 32-token half
     const int r = 16 * k + t;                // query-head row inside the tile
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
-    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    uint32_t n = 0;
+    const uint32_t lane_off = (uint32_t)(32 * k) << 16;
+    const uint32_t stat0 = BAR(stat) + 4 * r;
+    uint32_t n = 0, unit = 0;
     while (it.next(u)) {
-      // ---------------- Fused-Q-Quant prologue (a2): row r, content half h
+      // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh
+      if (unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // QK of the previous unit done
       float c_row;
       {
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
         float amax = 0.f;
 #pragma unroll
-        for (int bh = 0; bh < 2; ++bh) {
-          uint4 qv[16];
+        for (int bh = 0; bh < 4; ++bh) {
+          uint4 qv[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * h + 16 * bh + i) : make_uint4(0, 0, 0, 0);
+          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * hh + 8 * bh + i) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 8; ++i) {
             const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -383,179 +429,182 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 2
         for (int gch = 0; gch < 16; ++gch) {   // 16-byte chunk of codes (re-read: L1 hit)
           uint4 v2[2];
-          v2[0] = row_ok ? __ldg(qrow + 32 * h + 2 * gch) : make_uint4(0, 0, 0, 0);
-          v2[1] = row_ok ? __ldg(qrow + 32 * h + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+          v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
+          v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
           const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-          uint32_t w[4];
+          uint32_t wd[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-            w[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                             div_by(f1.y, sq, rsq));
+            wd[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                              div_by(f1.y, sq, rsq));
           }
-          const int byte = 256 * h + 16 * gch;          // byte offset inside the 512-B row
+          const int byte = 256 * hh + 16 * gch;          // byte offset inside the 512-B row
           const int sub = byte >> 7, c = (byte >> 4) & 7;
-          sts_u4(sbase + kOffQc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+          sts_u4(sbase + kOffQc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
         }
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
-          const uint4 v = row_ok ? __ldg(qrow + 64 + 4 * h + gch) : make_uint4(0, 0, 0, 0);
+          const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
+          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
           const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-          uint32_t w[4];
+          uint32_t wd[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = __bfloat1622float2(a[e]);
             __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
                                                    __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-            w[e] = *reinterpret_cast<uint32_t*>(&o2);
+            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
           }
-          const int c = 4 * h + gch;
-          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
         }
         fence_proxy_async_smem();
-        mbar_arrive(&bars.q_full);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(q_full));
       }
 
       const int L = __ldg(p.seq_lens + u.b);
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % kSlots;
-        mbar_wait(&bars.s_full[st], (n / kSlots) & 1, 7, n);
+        mbar_wait(BAR(s_full) + 8 * st, (n / kSlots) & 1, 7, n);
         tc_fence_after();
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         float tt[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_base + 64 * st, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * st, *reinterpret_cast<uint32_t(*)[32]>(tt));
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&bars.s_empty[st]);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
-
-        // sigma_K of my 32 tokens (from the TMA'd slot), kept in registers
-        const uint32_t sk = sbase + kOffKv + st * kStage + 5 * kBoxBytes + 128 * h;
-        const int nvalid = L - (j * kBc + 32 * h);   // tokens of my half inside the sequence
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(s_empty) + 8 * st);
+        // sigma_K of my 32 tokens (from the TMA'd slot)
+        const uint32_t sk = sbase + kOffKv + st * kStage + 5 * kBoxBytes + 128 * hh;
+        const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the sequence
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {                              // Alg.1 step 3 (descale)
-          const float4 s4 = lds_f4(sk + 4 * i);
-          const float2 a = __fmul2_rn(make_float2(tt[i], tt[i + 1]), make_float2(s4.x, s4.y));
-          const float2 b = __fmul2_rn(make_float2(tt[i + 2], tt[i + 3]), make_float2(s4.z, s4.w));
-          tt[i] = a.x;
-          tt[i + 1] = a.y;
-          tt[i + 2] = b.x;
-          tt[i + 3] = b.y;
+        for (int e = 0; e < 32; e += 4) {                              // Alg.1 step 3 (descale)
+          const float4 s4 = lds_f4(sk + 4 * e);
+          const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4.x, s4.y));
+          const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4.z, s4.w));
+          tt[e] = a.x;
+          tt[e + 1] = a.y;
+          tt[e + 2] = b.x;
+          tt[e + 3] = b.y;
         }
         if (nvalid < 32) {                                             // ragged tail block: mask (R19)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) tt[i] = i < nvalid ? tt[i] : -INFINITY;
+          for (int e = 0; e < 32; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
         }
-        float mx0 = fmaxf(tt[0], tt[1]), mx1 = fmaxf(tt[2], tt[3]);
+        float mx0 = fmaxf(fmaxf(tt[0], tt[1]), tt[2]), mx1 = fmaxf(fmaxf(tt[3], tt[4]), tt[5]);
 #pragma unroll
-        for (int i = 4; i < 32; i += 4) {
-          mx0 = fmaxf(mx0, fmaxf(tt[i], tt[i + 1]));
-          mx1 = fmaxf(mx1, fmaxf(tt[i + 2], tt[i + 3]));
+        for (int e = 6; e < 30; e += 4) {
+          mx0 = fmaxf(fmaxf(mx0, tt[e]), tt[e + 1]);
+          mx1 = fmaxf(fmaxf(mx1, tt[e + 2]), tt[e + 3]);
         }
-        float mx = fmaxf(mx0, mx1);
+        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));          // block max of t (local m)
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S2, n);
         const float mc = mx * c_row;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
         float mb0 = 0.f, mb1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 s4 = lds_f4(sk + 4 * i);                        // sigma_K (re-read, LDS broadcast)
-          const float2 e0 = __ffma2_rn(make_float2(tt[i], tt[i + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
-          const float2 e1 = __ffma2_rn(make_float2(tt[i + 2], tt[i + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+        for (int e = 0; e < 32; e += 4) {
+          const float4 s4 = lds_f4(sk + 4 * e);                        // sigma_K (re-read, LDS broadcast)
+          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
           const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));   // step 5 (block reference)
           const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
           const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));           // step 6: p * sigma_K
           const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
-          ls[0] += p0.x;
-          ls[1] += p0.y;
-          ls[2] += p1.x;
-          ls[3] += p1.y;
-          tt[i] = w0.x;
-          tt[i + 1] = w0.y;
-          tt[i + 2] = w1.x;
-          tt[i + 3] = w1.y;
-          mb0 = fmaxf(mb0, fmaxf(w0.x, w0.y));
-          mb1 = fmaxf(mb1, fmaxf(w1.x, w1.y));
+          ls0 = __fadd2_rn(ls0, p0);
+          ls1 = __fadd2_rn(ls1, p1);
+          tt[e] = w0.x;
+          tt[e + 1] = w0.y;
+          tt[e + 2] = w1.x;
+          tt[e + 3] = w1.y;
+          mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
+          mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
         }
-        float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        float lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
         float mb = fmaxf(mb0, mb1);
         mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
         // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
         // P' = 0 and is skipped by the recurrence (R11)
         const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
+        const float2 inv2 = make_float2(inv, inv);
         uint32_t pw[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          pw[i] = cvt4_e4m3(tt[4 * i] * inv, tt[4 * i + 1] * inv, tt[4 * i + 2] * inv, tt[4 * i + 3] * inv);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
+        for (int e = 0; e < 8; ++e) {
+          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
+          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
+          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+        }
         // P' slot free once PV_L and PV_R of block n - kSlots completed
-        mbar_wait(&bars.p_empty[st], ((n / kSlots) & 1) ^ 1, 8, n);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
+        mbar_wait(BAR(p_empty) + 8 * st, ((n / kSlots) & 1) ^ 1, 8, n);
         // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
         const uint32_t pdst = sbase + kOffP + st * 4096 + r * 16;
-        sts_u4(pdst + (2 * h) * 1024, pw[0], pw[1], pw[2], pw[3]);
-        sts_u4(pdst + (2 * h + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
-        if (h == 0) {
-          sts_f32(smem_u32(&bars.stat[st][0][r]), mb > 0.f ? mc : -INFINITY);
-          sts_f32(smem_u32(&bars.stat[st][1][r]), __fdiv_rn(mb, 448.0f));
-          sts_f32(smem_u32(&bars.stat[st][2][r]), lsum);
+        sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
+        sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        if (hh == 0) {
+          const uint32_t sa = stat0 + st * (3 * 64 * 4);
+          sts_f32(sa, mb > 0.f ? mc : -INFINITY);
+          sts_f32(sa + 256, __fdiv_rn(mb, 448.0f));
+          sts_f32(sa + 512, lsum);
         }
         fence_proxy_async_smem();
-        mbar_arrive(&bars.p_full[st]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(p_full) + 8 * st);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
+      ++unit;
     }
   } else {
     regs_inc<kRegsAcc>();
     // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
-    const int half = warp >> 2;              // 0: O cols 0-255 (T_L), 1: cols 256-511 (T_R)
+    const uint32_t w = warp >> 2;            // 0: O cols 0-255 (L halves), 1: cols 256-511 (R halves)
     const int k = warp & 3;
     const int t = lane & 15, hh = lane >> 4;
     const int r = 16 * k + t;
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
-    const uint32_t taddr = tmem_T + ((uint32_t)(32 * k) << 16) + 256 * half;
+    const uint32_t lane_off = (uint32_t)(32 * k) << 16;
+    const uint32_t stat0 = BAR(stat) + 4 * r;
     uint32_t n = 0;
     while (it.next(u)) {
       const uint32_t n0 = n;
       // O holds sum_b (sig_b 2^{m_b - m_O}) P'_b V in units of sig_O 2^{m_O} (log2 units);
-      // l_run = sum_b l_b 2^{m_b - m_ref}.  This thread: row r, cols 256 half + 128 hh + [0, 128).
+      // l_run = sum_b l_b 2^{m_b - m_ref}.  This thread: row r, cols 256 w + 128 hh + [0, 128).
       float o[128];
+#pragma unroll
+      for (int e = 0; e < 128; ++e) o[e] = 0.f;   // the first block enters with gamma = 0
       float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % kSlots;
-        mbar_wait(&bars.p_full[st], (n / kSlots) & 1, 9, n);
-        if (threadIdx.x == 0) TRACE(TR_C0, n);
-        const float mb = lds_f32(smem_u32(&bars.stat[st][0][r]));
-        const float sb = lds_f32(smem_u32(&bars.stat[st][1][r]));
-        const float lb = lds_f32(smem_u32(&bars.stat[st][2][r]));
+        mbar_wait(BAR(p_full) + 8 * st, (n / kSlots) & 1, 9, n);
+        const uint32_t sa = stat0 + st * (3 * 64 * 4);
+        const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
         const float m_new = fmaxf(m_ref, mb);                          // step 4 (running max)
         // a block whose contributions are < 2^-64 of the running total is dropped
         // (Alg.1 loses it to fp32 underflow of exp(s - m)); so is a zero-max block
         const bool first = n == n0;
         const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
-        float gamma = 1.f;
+        float gamma = 0.f;
         if (first) {
           m_O = mb;
           sig_O = sb;
           l_run = lb;
           m_ref = mb;
         } else if (!skip) {
-          gamma = ex2_approx(m_O - mb) * __fdiv_rn(sig_O, sb);         // steps 9-10
+          gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);        // steps 9-10
           l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
           m_ref = m_new;
           m_O = mb;
           sig_O = sb;
         }
-        mbar_wait(&bars.t_full[half], n & 1, 10, n);                   // T(n) = P'(n) V complete
+        const uint32_t h = 2 * n + w, ts = h % kTSlots;
+        mbar_wait(BAR(t_full) + 8 * ts, (h / kTSlots) & 1, 10, n);      // T half = P'(n) V complete
         tc_fence_after();
-        if (threadIdx.x == 0) TRACE(TR_C1, n);
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
+        const uint32_t taddr = t_slot_addr(tmem, ts) + lane_off;
         const float2 g2 = make_float2(gamma, gamma);
-        // software-pipelined T reads (8 chunks of 16 columns): chunk c+1 is in
-        // flight while chunk c is FMA'd
+        // software-pipelined T reads (8 chunks of 16 columns)
         uint32_t tv[2][16];
         tmem_ld_16x32bx2_x16<128>(taddr, tv[0]);
 #pragma unroll
@@ -564,38 +613,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c < 7) tmem_ld_16x32bx2_x16<128>(taddr + 16 * (c + 1), tv[(c + 1) & 1]);
           else {
             tc_fence_before();
-            mbar_arrive(&bars.t_free[half]);                           // PV(n+1) may overwrite T
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(t_free) + 8 * ts);           // PV may overwrite the slot
           }
           const uint32_t* cur = tv[c & 1];
-          if (first) {
+          if (!skip) {   // first block: gamma = 0 on a zeroed O
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[16 * c + i] = __uint_as_float(cur[i]);
-          } else if (!skip) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-              const float2 a = __ffma2_rn(make_float2(o[16 * c + i], o[16 * c + i + 1]), g2,
-                                          make_float2(__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])));
-              o[16 * c + i] = a.x;
-              o[16 * c + i + 1] = a.y;
+            for (int e = 0; e < 16; e += 2) {
+              const float2 a = __ffma2_rn(make_float2(o[16 * c + e], o[16 * c + e + 1]), g2,
+                                          make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
+              o[16 * c + e] = a.x;
+              o[16 * c + e + 1] = a.y;
             }
           }
         }
-        if (threadIdx.x == 0) TRACE(TR_C_L, n);
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
       }
       // ---------------- epilogue (a9): o = sig_O 2^{m_O - m_ref} O / l ; L = (m_ref + log2 l) ln 2
       const float f = sig_O * ex2_approx(m_O - m_ref) / l_run;
       const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
       if (row_ok) {
-        float* dst = p.o_part + prow * kDc + 256 * half + 128 * hh;
+        float* dst = p.o_part + prow * kDc + 256 * w + 128 * hh;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          // chunk c of this thread = TMEM cols [32c, 32c+32) (+128 for threads 16-31)
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + 32 * c + i) =
-                make_float4(o[32 * c + i] * f, o[32 * c + i + 1] * f, o[32 * c + i + 2] * f, o[32 * c + i + 3] * f);
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + 32 * c + e) =
+                make_float4(o[32 * c + e] * f, o[32 * c + e + 1] * f, o[32 * c + e + 2] * f, o[32 * c + e + 3] * f);
         }
-        if (half == 0 && hh == 0) p.lse_part[prow] = (m_ref + log2f(l_run)) * 0.69314718055994531f;
+        if (w == 0 && hh == 0) p.lse_part[prow] = (m_ref + log2f(l_run)) * 0.69314718055994531f;
       }
     }
   }
@@ -606,11 +652,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+#ifdef SNAPMLA_TRACE
   if (p.trace != nullptr && threadIdx.x == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
     p.trace[TR_NEV * kTraceN + 2 * blockIdx.x + 1] = gt;
   }
+#endif
 }
 
 // ------------------------------------------------------------------ host side

@@ -27,8 +27,20 @@ DEVI void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef SNAPMLA_SUSPEND_NS
+#define SNAPMLA_SUSPEND_NS 0
+#endif
 DEVI bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if SNAPMLA_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "n"(SNAPMLA_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
@@ -36,6 +48,7 @@ DEVI bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 #ifdef SNAPMLA_HANG_CHECK
@@ -58,10 +71,48 @@ DEVI void mbar_wait(uint64_t* bar, uint32_t parity, int = -1, int = -1) {
 }
 #endif
 
+// u32 shared-window address variants (no generic->shared conversion at the call site)
+DEVI void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+DEVI void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+DEVI void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+#ifdef SNAPMLA_HANG_CHECK
+DEVI void mbar_wait(uint32_t a, uint32_t parity, int tag = -1, int idx = -1) {
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << 31)) {
+      printf("HANG block %d thread %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x, tag, idx, parity);
+      __trap();
+    }
+  }
+}
+#else
+DEVI void mbar_wait(uint32_t a, uint32_t parity, int = -1, int = -1) {
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+#endif
+// producer-side wait (not latency critical): back off between probes so the
+// spinning warp leaves issue slots to the compute warps
+DEVI void mbar_wait_backoff(uint32_t a, uint32_t parity) {
+  while (!mbar_try_wait(a, parity)) __nanosleep(64);
+}
+
 // ------------------------------------------------------- shared-space access
 DEVI float4 lds_f4(uint32_t saddr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
+DEVI uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
   return v;
 }
 DEVI float lds_f32(uint32_t saddr) {
@@ -102,6 +153,19 @@ DEVI void tma_load_2d(uint32_t dst, const void* desc, uint64_t* bar, int32_t x, 
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+DEVI void tma_load_2d(uint32_t dst, const void* desc, uint32_t bar, int32_t x, int32_t y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+DEVI void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
 DEVI void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
@@ -119,6 +183,11 @@ DEVI uint64_t l2_policy_evict_first() {
 DEVI void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+DEVI void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
@@ -154,6 +223,13 @@ DEVI void mma_commit_ws(uint64_t* bar) {
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+DEVI void mma_commit_ws(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]^T, FP8 E4M3 x E4M3 -> FP32
@@ -243,6 +319,17 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t a_fmt, uint32_t b_fmt
 DEVI uint16_t cvt_e4m3x2(float lo, float hi) {
   uint16_t r;
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// four fp32 -> four E4M3 bytes (a lowest), RNE, satfinite
+DEVI uint32_t cvt4_e4m3(float a, float b, float c, float d) {
+  uint32_t r;
+  asm("{\n\t.reg .b16 lo, hi;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n\t"
+      "mov.b32 %0, {lo, hi};\n\t}"
+      : "=r"(r)
+      : "f"(a), "f"(b), "f"(c), "f"(d));
   return r;
 }
 DEVI float ex2_approx(float x) {

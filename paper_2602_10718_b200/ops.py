@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsnapmla.so")
+LIB_PATH = os.environ.get("SNAPMLA_LIB", os.path.join(_HERE, "libsnapmla.so"))   # override: experiments only
 _lib = None
 
 D_C, D_R, PAGE = 512, 64, 64

@@ -22,7 +22,7 @@ q = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
 sl = torch.full((B,), L, dtype=torch.int32, device=dev)
 NEV = 16
 tr = torch.zeros(NEV * 256 + 2 * 1024, dtype=torch.int64, device=dev)
-lib = ops.lib()
+lib = ops.lib()  # use SNAPMLA_LIB=...libsnapmla_trace.so (SNAPMLA_TRACE build)
 lib.mla_debug_set_trace.argtypes = [ctypes.c_void_p]
 for i in range(3):
     if i == 2:
