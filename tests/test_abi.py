@@ -47,7 +47,7 @@ def test_sass_is_sm100a_tcgen05_tma(L):
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", ops.LIB_PATH], capture_output=True,
                           text=True).stdout
     assert "sm_100a" in sass
-    for mnem in ("UTCQMMA", "UTCHMMA", "UTMALDG", "LDTM", "STTM"):
+    for mnem in ("UTCQMMA", "UTCHMMA", "UTMALDG", "LDTM", "UTCBAR"):
         assert mnem in sass, mnem
 
 
