@@ -49,15 +49,16 @@ constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
 constexpr int kWarpSoftmax = 12;  // 12-15 softmax
 // register budget (setmaxnreg): 256 x 192 + 128 x 40 + 128 x 88 = 65,536 = 512 x 128 (launch)
 constexpr uint32_t kRegsAcc = 192, kRegsIssue = 40, kRegsSoftmax = 88;
-constexpr int kSlots = 4;         // KV / S / P' ring depth (blocks)
+constexpr int kSlots = 4;         // KV / P' ring depth (blocks)
+constexpr int kSSlots = 2;        // S ring depth (TMEM)
 constexpr int kTSlots = 3;        // TMEM ring of 64 x 256 PV half tiles
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
 constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
-constexpr uint32_t kOffQc = 0;                              // 4 x [64 rows x 128 B] SW128
-constexpr uint32_t kOffQr = 32768;                          // [64 rows x 128 B] SW128
-constexpr uint32_t kOffP = 40960;                           // 4 slots x 4096 B, K-major core matrices
-constexpr uint32_t kOffKv = 57344;                          // 4 slots: 4 content boxes | RoPE box | scales
+constexpr uint32_t kOffQr = 0;                              // [64 rows x 128 B] SW128 (q_r / sigma_q, BF16)
+constexpr uint32_t kOffP = 8192;                            // 4 slots x 4096 B, K-major core matrices
+constexpr uint32_t kOffKv = 24576;                          // 4 slots: 4 content boxes | RoPE box | scales
+constexpr uint32_t kOffScaleHi = 5 * 8192 + 144;            // sigma_K of tokens 32-63 (bank-shifted by 16 B)
 constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
 constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
 static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -99,7 +100,7 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
 
 struct Bars {
   uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
-  uint64_t s_full[kSlots], s_empty[kSlots];     // QK -> softmax WG / softmax WG -> QK
+  uint64_t s_full[kSSlots], s_empty[kSSlots];   // QK -> softmax / softmax -> QK
   uint64_t p_full[kSlots], p_empty[kSlots];     // P' + stats: softmax WG -> PV, WGs / PV_L + PV_R -> softmax
   uint64_t t_full[kTSlots], t_free[kTSlots];    // T ring: PV -> WG / WG -> PV
   uint64_t q_full, q_free;                      // Q-quant prologue -> QK / QK of a unit done -> prologue
@@ -226,25 +227,26 @@ __device__ __forceinline__ float div_by(float x, float s, float rs) {
 // then 4 x kind::f16 (K = 16) over the 64 RoPE dims, accumulating into the same S;
 // commit to `bar`.  One elect for the whole block.  Descriptor start addresses
 // advance in 16-byte units: content step kk at byte (kk / 4) * 8192 + (kk % 4) * 32.
-#define SNAPMLA_QK8(ao, acc)                                                                   \
-  "add.s64 a, %1, " #ao ";\n\tadd.s64 b, %2, " #ao ";\n\t"                                     \
-  "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, " acc ";\n\t"
+#define SNAPMLA_QK8(ta, bo, acc)                                                               \
+  "add.u32 t, %1, " #ta ";\n\tadd.s64 b, %2, " #bo ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [t], b, %3, " acc ";\n\t"
 #define SNAPMLA_QK16(ao)                                                                       \
   "add.s64 a, %4, " #ao ";\n\tadd.s64 b, %5, " #ao ";\n\t"                                     \
   "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, pt;\n\t"
-__device__ __forceinline__ void qk_issue(uint32_t dS, uint64_t dQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
+// The content A operand (q_c codes) lives in TMEM: step kk reads columns tQ + 8 kk.
+__device__ __forceinline__ void qk_issue(uint32_t dS, uint32_t tQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
                                          uint32_t bar) {
   asm volatile(
-      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, t;\n\t"
       "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      SNAPMLA_QK8(0, "pf") SNAPMLA_QK8(2, "pt") SNAPMLA_QK8(4, "pt") SNAPMLA_QK8(6, "pt")
-      SNAPMLA_QK8(512, "pt") SNAPMLA_QK8(514, "pt") SNAPMLA_QK8(516, "pt") SNAPMLA_QK8(518, "pt")
-      SNAPMLA_QK8(1024, "pt") SNAPMLA_QK8(1026, "pt") SNAPMLA_QK8(1028, "pt") SNAPMLA_QK8(1030, "pt")
-      SNAPMLA_QK8(1536, "pt") SNAPMLA_QK8(1538, "pt") SNAPMLA_QK8(1540, "pt") SNAPMLA_QK8(1542, "pt")
+      SNAPMLA_QK8(0, 0, "pf") SNAPMLA_QK8(8, 2, "pt") SNAPMLA_QK8(16, 4, "pt") SNAPMLA_QK8(24, 6, "pt")
+      SNAPMLA_QK8(32, 512, "pt") SNAPMLA_QK8(40, 514, "pt") SNAPMLA_QK8(48, 516, "pt") SNAPMLA_QK8(56, 518, "pt")
+      SNAPMLA_QK8(64, 1024, "pt") SNAPMLA_QK8(72, 1026, "pt") SNAPMLA_QK8(80, 1028, "pt") SNAPMLA_QK8(88, 1030, "pt")
+      SNAPMLA_QK8(96, 1536, "pt") SNAPMLA_QK8(104, 1538, "pt") SNAPMLA_QK8(112, 1540, "pt") SNAPMLA_QK8(120, 1542, "pt")
       SNAPMLA_QK16(0) SNAPMLA_QK16(2) SNAPMLA_QK16(4) SNAPMLA_QK16(6)
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}"
-      ::"r"(dS), "l"(dQ), "l"(dK), "r"(kIdescQk8), "l"(dQr), "l"(dKr), "r"(kIdescQk16), "r"(bar)
+      ::"r"(dS), "r"(tQ), "l"(dK), "r"(kIdescQk8), "l"(dQr), "l"(dKr), "r"(kIdescQk16), "r"(bar)
       : "memory");
 }
 
@@ -266,8 +268,13 @@ __device__ __forceinline__ void pv_issue(uint32_t dT, uint64_t dP, uint64_t dV, 
       : "memory");
 }
 
+// TMEM map (M = 64 data-path layout: row m at lane (m % 16) + 32 (m / 16), +16 for the
+// upper half-subpartitions).  Lanes 0-15: S slots 0 / 1 (cols 0 / 64), the Q content codes
+// (cols 128-255, the QK A operand: A-in-TMEM must start at lane 0, scripts/tmem_a_check.cu),
+// T slot 0 (cols 256-511).  Lanes 16-31: T slots 1 / 2 (cols 0 / 256).
+constexpr uint32_t kTmemQ = 128;
 __device__ __forceinline__ uint32_t t_slot_addr(uint32_t tmem, uint32_t s) {
-  return tmem + (s == 2 ? (16u << 16) + 256u : 256u * s);
+  return tmem + (s == 0 ? 256u : (16u << 16) + 256u * (s - 1));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -283,10 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(BAR(kv_full) + 8 * i, 1);
       mbar_init(BAR(kv_empty) + 8 * i, 2);
+      mbar_init(BAR(p_full) + 8 * i, 4);
+      mbar_init(BAR(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
+    }
+    for (int i = 0; i < kSSlots; ++i) {
       mbar_init(BAR(s_full) + 8 * i, 1);
       mbar_init(BAR(s_empty) + 8 * i, 4);
-      mbar_init(BAR(p_full) + 8 * i, 4);
-      mbar_init(BAR(p_empty) + 8 * i, 2);
     }
     for (int i = 0; i < kTSlots; ++i) {
       mbar_init(BAR(t_full) + 8 * i, 1);
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = lds_u32(BAR(tmem_base));
-  const uint32_t tmem_S = tmem + (16u << 16);         // lanes 16-31 (+32k): S slot s at cols 64 s
+  const uint32_t tmem_S = tmem;                       // lanes 0-15 (+32k): S slot s at cols 64 s
 
   pdl_wait();   // plan (and the appends before it) visible from here on
   const int ht = blockIdx.x % p.n_ht;
@@ -345,28 +354,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, full, c * 128, row, pol);
             tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, full, 0, row, pol);
-            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 256, full, pol);
+            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 128, full, pol);
+            bulk_load(dst + kOffScaleHi, p.kv_scale + (int64_t)row + 32, 128, full, pol);
           }
         }
       }
     } else if (warp == kWarpQk) {
       // ================================ QK issuer ================================
-      const uint64_t dQ = make_smem_desc(sbase + kOffQc, 16, 1024, LAYOUT_SW128);
       const uint64_t dQr = make_smem_desc(sbase + kOffQr, 16, 1024, LAYOUT_SW128);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
         mbar_wait(BAR(q_full), unit & 1, 2, unit);
         for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kSlots;
+          const uint32_t st = n % kSlots, ss = n % kSSlots;
           mbar_wait(BAR(kv_full) + 8 * st, (n / kSlots) & 1, 3, n);
-          mbar_wait(BAR(s_empty) + 8 * st, ((n / kSlots) & 1) ^ 1, 4, n);
+          mbar_wait(BAR(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
           tc_fence_after();
           if (lane == 0) TRACE(TR_QK, n);
           const uint32_t kv = sbase + kOffKv + st * kStage;
-          qk_issue(tmem_S + 64 * st, dQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
-                   make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * st);
+          qk_issue(tmem_S + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                   make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
         }
-        mma_commit_ws(BAR(q_free));   // Q SMEM reusable once this unit's QK MMAs completed
+        mma_commit_ws(BAR(q_free));   // Q (TMEM + SMEM) reusable once this unit's QK MMAs completed
         ++unit;
       }
     } else {
@@ -426,23 +435,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
         c_row = sq * p.scale_log2;
-#pragma unroll 2
-        for (int gch = 0; gch < 16; ++gch) {   // 16-byte chunk of codes (re-read: L1 hit)
-          uint4 v2[2];
-          v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
-          v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-          uint32_t wd[4];
+        // q_c codes -> TMEM (the QK A operand): this thread's 256 content bytes are TMEM
+        // columns kTmemQ + 64 hh + [0, 64) of its row, 4 codes per column (low byte first)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-            wd[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                              div_by(f1.y, sq, rsq));
+        for (int half32 = 0; half32 < 2; ++half32) {
+          uint32_t qa[32];
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {   // 16-byte chunk of codes (re-read: L1 hit)
+            const int gch = 8 * half32 + g8;
+            uint4 v2[2];
+            v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
+            v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+              qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                                         div_by(f1.y, sq, rsq));
+            }
           }
-          const int byte = 256 * hh + 16 * gch;          // byte offset inside the 512-B row
-          const int sub = byte >> 7, c = (byte >> 4) & 7;
-          sts_u4(sbase + kOffQc + sub * 8192 + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+          tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
         }
+        tmem_wait_st();
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
           const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
@@ -459,24 +473,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
         }
         fence_proxy_async_smem();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(q_full));
       }
 
       const int L = __ldg(p.seq_lens + u.b);
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % kSlots;
-        mbar_wait(BAR(s_full) + 8 * st, (n / kSlots) & 1, 7, n);
+        const uint32_t st = n % kSlots, ss = n % kSSlots;
+        mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
         tc_fence_after();
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         float tt[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * st, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(s_empty) + 8 * st);
+        if (lane == 0) mbar_arrive(BAR(s_empty) + 8 * ss);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
         // sigma_K of my 32 tokens (from the TMA'd slot)
-        const uint32_t sk = sbase + kOffKv + st * kStage + 5 * kBoxBytes + 128 * hh;
+        const uint32_t sk = sbase + kOffKv + st * kStage + (hh ? kOffScaleHi : 5 * kBoxBytes);
         const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the sequence
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {                              // Alg.1 step 3 (descale)
@@ -500,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));          // block max of t (local m)
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S2, n);
         const float mc = mx * c_row;
         float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
         float mb0 = 0.f, mb1 = 0.f;
@@ -525,8 +542,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mb = fmaxf(mb0, mb1);
         mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
         // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
         // P' = 0 and is skipped by the recurrence (R11)
+        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
         const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
         const float2 inv2 = make_float2(inv, inv);
         uint32_t pw[8];
@@ -536,18 +555,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
           pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
         }
-        // P' slot free once PV_L and PV_R of block n - kSlots completed
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
+        // P' / stats slot free once PV_L and PV_R of block n - kSlots completed and the
+        // eight accumulator warps read its stats
         mbar_wait(BAR(p_empty) + 8 * st, ((n / kSlots) & 1) ^ 1, 8, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
         // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
+        if (hh == 0) {
+          const uint32_t sa = stat0 + st * (3 * 64 * 4);
+          sts_f32(sa, st_m);
+          sts_f32(sa + 256, st_sig);
+          sts_f32(sa + 512, lsum);
+        }
         const uint32_t pdst = sbase + kOffP + st * 4096 + r * 16;
         sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
         sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
-        if (hh == 0) {
-          const uint32_t sa = stat0 + st * (3 * 64 * 4);
-          sts_f32(sa, mb > 0.f ? mc : -INFINITY);
-          sts_f32(sa + 256, __fdiv_rn(mb, 448.0f));
-          sts_f32(sa + 512, lsum);
-        }
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_C2, n);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(p_full) + 8 * st);
@@ -580,6 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(BAR(p_full) + 8 * st, (n / kSlots) & 1, 9, n);
         const uint32_t sa = stat0 + st * (3 * 64 * 4);
         const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(p_empty) + 8 * st);             // stats of this slot consumed
         const float m_new = fmaxf(m_ref, mb);                          // step 4 (running max)
         // a block whose contributions are < 2^-64 of the running total is dropped
         // (Alg.1 loses it to fp32 underflow of exp(s - m)); so is a zero-max block

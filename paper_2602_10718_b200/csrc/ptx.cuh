@@ -100,8 +100,85 @@ DEVI void mbar_wait(uint32_t a, uint32_t parity, int = -1, int = -1) {
 #endif
 // producer-side wait (not latency critical): back off between probes so the
 // spinning warp leaves issue slots to the compute warps
+#ifndef SNAPMLA_BACKOFF_NS
+#define SNAPMLA_BACKOFF_NS 256
+#endif
 DEVI void mbar_wait_backoff(uint32_t a, uint32_t parity) {
-  while (!mbar_try_wait(a, parity)) __nanosleep(64);
+  while (!mbar_try_wait(a, parity)) __nanosleep(SNAPMLA_BACKOFF_NS);
+}
+
+// ------------------------------------------------------------- clusters
+DEVI uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address of this CTA -> shared::cluster address of the same offset in CTA `rank`
+DEVI uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+DEVI void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+DEVI void st_cluster_u4(uint32_t caddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+DEVI void st_cluster_f32(uint32_t caddr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(caddr), "f"(v) : "memory");
+}
+// arrive (release at cluster scope) on an mbarrier given by its shared::cluster address
+DEVI void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+DEVI bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait (acquire at cluster scope) for a phase that may include remote arrivals
+DEVI void mbar_wait_cluster(uint32_t a, uint32_t parity, int tag = -1, int idx = -1) {
+#ifdef SNAPMLA_HANG_CHECK
+  const long long t0 = clock64();
+  while (!mbar_try_wait_cluster(a, parity)) {
+    if (clock64() - t0 > (1ll << 31)) {
+      printf("HANG(c) block %d thread %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x, tag, idx, parity);
+      __trap();
+    }
+  }
+#else
+  while (!mbar_try_wait_cluster(a, parity)) {
+  }
+#endif
+}
+DEVI void fence_proxy_async_cluster() { asm volatile("fence.proxy.async.shared::cluster;" ::: "memory"); }
+// arrive + expect_tx (release at cluster scope) on a peer CTA's mbarrier
+DEVI void mbar_arrive_expect_tx_cluster(uint32_t caddr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(caddr), "r"(bytes)
+               : "memory");
+}
+// relaxed remote arrive: a pure signal (no data published through it).  A release
+// at cluster scope costs ~2,000 cycles (measured), so data always travels through
+// a bulk copy's complete_tx, and arrives whose only job is "slot consumed" (the
+// reads it guards completed: their values were used before the arrive) are relaxed.
+DEVI void mbar_arrive_cluster_relaxed(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// bulk async copy from this CTA's SMEM into a peer CTA's SMEM (TMA engine), completing
+// `bytes` of transaction count on the peer's mbarrier
+DEVI void bulk_copy_s2c(uint32_t dst_caddr, uint32_t src, uint32_t bytes, uint32_t bar_caddr) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_caddr),
+      "r"(src), "r"(bytes), "r"(bar_caddr)
+      : "memory");
 }
 
 // ------------------------------------------------------- shared-space access
@@ -280,6 +357,26 @@ DEVI void tmem_ld_16x32bx2_x16(uint32_t taddr, uint32_t (&r)[16]) {
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr), "n"(SPLIT));
+}
+// 32 lanes x N columns: thread i reads lane base+i, columns [col, col+N)
+DEVI void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DEVI void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 template <int SPLIT>
 DEVI void tmem_st_16x32bx2_x32(uint32_t taddr, const uint32_t (&r)[32]) {

@@ -129,3 +129,30 @@ def test_deterministic_bitwise():
     o2, l2 = case.gpu_decode(cache, f32_out=True)
     assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
     assert np.array_equal(l1.view(np.uint32), l2.view(np.uint32))
+
+
+# ---- H in (64, 128]: two 64-row head tiles per key block (padded tile for H < 128)
+@pytest.mark.parametrize("lens", [[1], [2, 63], [64, 65, 127, 128, 129], [4096 + 17], [0, 300, 0, 7],
+                                  [148 * 64 + 3, 5]])
+@pytest.mark.parametrize("H", [128, 96, 65])
+def test_two_head_tiles(H, lens):
+    heads = np.unique(np.array([0, 1, 31, 32, 63, 64, 95, H - 1]) % H)
+    case = Case(lens, H, seed=100 + H + len(lens))
+    out, lse = _check(case, heads_per_req=heads)
+    for b, L in enumerate(lens):
+        if L == 0:
+            assert np.all(out[b] == 0) and np.all(np.isneginf(lse[b]))
+
+
+def test_two_head_tiles_many_requests_all_heads():
+    rng = np.random.default_rng(21)
+    lens = rng.integers(0, 1500, 29)
+    _check(Case(lens, 128, seed=22))
+
+
+def test_two_head_tiles_deterministic_bitwise():
+    case = Case([5000, 65, 1], 128, seed=23)
+    cache = case.gpu_cache()
+    o1, _ = case.gpu_decode(cache, f32_out=True)
+    o2, _ = case.gpu_decode(cache, f32_out=True)
+    assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
