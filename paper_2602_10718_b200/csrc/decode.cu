@@ -47,17 +47,19 @@ constexpr int kWarpTma = 8;       // 8     TMA producer
 constexpr int kWarpQk = 9;        // 9     QK issuer, owns TMEM
 constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
 constexpr int kWarpSoftmax = 12;  // 12-15 softmax
-// register budget (setmaxnreg): 256 x 192 + 128 x 40 + 128 x 88 = 65,536 = 512 x 128 (launch)
-constexpr uint32_t kRegsAcc = 192, kRegsIssue = 40, kRegsSoftmax = 88;
-constexpr int kSlots = 4;         // KV / P' ring depth (blocks)
+// register budget (setmaxnreg; balanced per SMSP: 2 acc + 1 issue + 1 softmax warp each):
+// 256 x 176 + 128 x 40 + 128 x 120 = 65,536 = 512 x 128 (launch)
+constexpr uint32_t kRegsAcc = 176, kRegsIssue = 40, kRegsSoftmax = 120;
+constexpr int kSlots = 5;         // KV ring depth (blocks)
+constexpr int kPSlots = 2;        // P' + stats ring depth (blocks)
 constexpr int kSSlots = 2;        // S ring depth (TMEM)
 constexpr int kTSlots = 3;        // TMEM ring of 64 x 256 PV half tiles
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
 constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
 constexpr uint32_t kOffQr = 0;                              // [64 rows x 128 B] SW128 (q_r / sigma_q, BF16)
-constexpr uint32_t kOffP = 8192;                            // 4 slots x 4096 B, K-major core matrices
-constexpr uint32_t kOffKv = 24576;                          // 4 slots: 4 content boxes | RoPE box | scales
+constexpr uint32_t kOffP = 8192;                            // 2 slots x 4096 B, K-major core matrices
+constexpr uint32_t kOffKv = 16384;                          // 5 slots: 4 content boxes | RoPE box | scales
 constexpr uint32_t kOffScaleHi = 5 * 8192 + 144;            // sigma_K of tokens 32-63 (bank-shifted by 16 B)
 constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
 constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
@@ -101,11 +103,11 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
 struct Bars {
   uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
   uint64_t s_full[kSSlots], s_empty[kSSlots];   // QK -> softmax / softmax -> QK
-  uint64_t p_full[kSlots], p_empty[kSlots];     // P' + stats: softmax WG -> PV, WGs / PV_L + PV_R -> softmax
+  uint64_t p_full[kPSlots], p_empty[kPSlots];   // P' + stats: softmax -> PV, acc / PV_L + PV_R + acc -> softmax
   uint64_t t_full[kTSlots], t_free[kTSlots];    // T ring: PV -> WG / WG -> PV
   uint64_t q_full, q_free;                      // Q-quant prologue -> QK / QK of a unit done -> prologue
   uint32_t tmem_base;
-  float stat[kSlots][3][64];          // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
+  float stat[kPSlots][3][64];         // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
 };
 static_assert(sizeof(Bars) <= 4096, "barrier region");
 #define BAR(field) (bar0 + (uint32_t)offsetof(Bars, field))
@@ -290,6 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(BAR(kv_full) + 8 * i, 1);
       mbar_init(BAR(kv_empty) + 8 * i, 2);
+    }
+    for (int i = 0; i < kPSlots; ++i) {
       mbar_init(BAR(p_full) + 8 * i, 4);
       mbar_init(BAR(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
     }
@@ -384,17 +388,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t n = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kSlots;
+          const uint32_t st = n % kSlots, ps = n % kPSlots;
           const uint32_t h = 2 * n + half, ts = h % kTSlots;
-          mbar_wait(BAR(p_full) + 8 * st, (n / kSlots) & 1, 5, n);                   // P'(n) in SMEM
+          mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);                  // P'(n) in SMEM
           if (h >= kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / kTSlots - 1) & 1, 6, n);   // slot read
           tc_fence_after();
           if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
-          const uint32_t pA = sbase + kOffP + st * 4096;
+          const uint32_t pA = sbase + kOffP + ps * 4096;
           const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
           pv_issue(t_slot_addr(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
                    make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
-                   BAR(p_empty) + 8 * st, BAR(kv_empty) + 8 * st);
+                   BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
         }
       }
     }
@@ -479,13 +483,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 
       const int L = __ldg(p.seq_lens + u.b);
+      // S(n) is loaded from TMEM one block ahead: the load of S(n+1) is issued before
+      // block n's P' / stats stores, fence and arrive, which hide its latency.
+      float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % kSlots, ss = n % kSSlots;
-        mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
-        tc_fence_after();
+        const uint32_t st = n % kSlots, ss = n % kSSlots, ps = n % kPSlots;
+        if (j == u.k0) {
+          mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
+          tc_fence_after();
+          tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
-        float tt[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -494,9 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // sigma_K of my 32 tokens (from the TMA'd slot)
         const uint32_t sk = sbase + kOffKv + st * kStage + (hh ? kOffScaleHi : 5 * kBoxBytes);
         const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the sequence
+        float4 skv[8];                                                 // sigma_K of my 32 tokens, kept
+#pragma unroll
+        for (int e = 0; e < 8; ++e) skv[e] = lds_f4(sk + 16 * e);
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {                              // Alg.1 step 3 (descale)
-          const float4 s4 = lds_f4(sk + 4 * e);
+          const float4 s4 = skv[e / 4];
           const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4.x, s4.y));
           const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4.z, s4.w));
           tt[e] = a.x;
@@ -522,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mb0 = 0.f, mb1 = 0.f;
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 s4 = lds_f4(sk + 4 * e);                        // sigma_K (re-read, LDS broadcast)
+          const float4 s4 = skv[e / 4];
           const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
           const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
           const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));   // step 5 (block reference)
@@ -556,24 +567,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
         }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
-        // P' / stats slot free once PV_L and PV_R of block n - kSlots completed and the
+        if (j + 1 < u.k1) {   // prefetch S(n+1)
+          const uint32_t ss1 = (n + 1) % kSSlots;
+          mbar_wait(BAR(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
+          tc_fence_after();
+          tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
+        // P' / stats slot free once PV_L and PV_R of block n - kPSlots completed and the
         // eight accumulator warps read its stats
-        mbar_wait(BAR(p_empty) + 8 * st, ((n / kSlots) & 1) ^ 1, 8, n);
+        mbar_wait(BAR(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
         // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
         if (hh == 0) {
-          const uint32_t sa = stat0 + st * (3 * 64 * 4);
+          const uint32_t sa = stat0 + ps * (3 * 64 * 4);
           sts_f32(sa, st_m);
           sts_f32(sa + 256, st_sig);
           sts_f32(sa + 512, lsum);
         }
-        const uint32_t pdst = sbase + kOffP + st * 4096 + r * 16;
+        const uint32_t pdst = sbase + kOffP + ps * 4096 + r * 16;
         sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
         sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_C2, n);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(p_full) + 8 * st);
+        if (lane == 0) mbar_arrive(BAR(p_full) + 8 * ps);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
       ++unit;
@@ -599,12 +616,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < 128; ++e) o[e] = 0.f;   // the first block enters with gamma = 0
       float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % kSlots;
-        mbar_wait(BAR(p_full) + 8 * st, (n / kSlots) & 1, 9, n);
-        const uint32_t sa = stat0 + st * (3 * 64 * 4);
+        const uint32_t ps = n % kPSlots;
+        mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        const uint32_t sa = stat0 + ps * (3 * 64 * 4);
         const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(p_empty) + 8 * st);             // stats of this slot consumed
+        if (lane == 0) mbar_arrive(BAR(p_empty) + 8 * ps);             // stats of this slot consumed
         const float m_new = fmaxf(m_ref, mb);                          // step 4 (running max)
         // a block whose contributions are < 2^-64 of the running total is dropped
         // (Alg.1 loses it to fp32 underflow of exp(s - m)); so is a zero-max block
