@@ -64,6 +64,8 @@ constexpr uint32_t kOffScaleHi = 5 * 8192 + 144;            // sigma_K of tokens
 constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
 constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
 static_assert(kSmemBytes <= 232448, "shared memory budget");
+static_assert(2 * 32 * kRegsAcc + 32 * kRegsIssue + 32 * kRegsSoftmax <= 4 * 32 * 128,
+              "setmaxnreg budget per SMSP (launch: 4 warps x 128 registers)");
 
 // instruction descriptors (M = 64)
 constexpr uint32_t kIdescQk8 = make_idesc(0, 0, 0, 0, 64, 64);      // E4M3 x E4M3, both K-major
@@ -403,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kWarpSoftmax) {
-    regs_dec<kRegsSoftmax>();
+    if constexpr (kRegsSoftmax > 128) regs_inc<kRegsSoftmax>();   // launch: 128 per thread
+    else regs_dec<kRegsSoftmax>();
     // ======= softmax / scale fusion / P quantization: thread = (row, 32-token half) =======
     const int k = warp & 3;                  // TMEM subpartition of this warp
     const int t = lane & 15, hh = lane >> 4; // row-in-quarter, 32-token half
@@ -596,7 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++unit;
     }
   } else {
-    regs_inc<kRegsAcc>();
+    if constexpr (kRegsAcc > 128) regs_inc<kRegsAcc>();
+    else regs_dec<kRegsAcc>();
     // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
     const uint32_t w = warp >> 2;            // 0: O cols 0-255 (L halves), 1: cols 256-511 (R halves)
     const int k = warp & 3;
