@@ -9,6 +9,7 @@
  *                        (Eq.5, §3.2, Algorithm 1 P:666-744,
  *                        Appendix C order enforcement P:759-764); Q quantization
  *                        (Fused-Q-Quant) runs in its prologue
+ *   mla_decode_fp8_ex    the same with q_len query tokens per request (MTP)
  *   mla_combine          split-KV merge of the per-split (o, logsumexp) partials
  *                        (Algorithm 1 returns o and L)
  *
@@ -117,6 +118,26 @@ mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const void* kv_r
                           int kv_lora_rank, int rope_dim, int page_size, int max_pages_per_seq,
                           int64_t num_pages, float softmax_scale, void* workspace, size_t workspace_bytes,
                           mla_stream_t stream);
+
+/*
+ * mla_decode_fp8_ex -- the same decode with q_len >= 1 query tokens per request
+ * (multi-token prediction, MTP; the paper evaluates MTP in {1, 2}).
+ *
+ *   q          bf16 [batch, q_len, num_heads, 576]; row (t, h) = t * num_heads + h
+ *   query token t (0-based) sits at position seq_lens[b] - q_len + t and attends to
+ *   keys 0 .. seq_lens[b] - q_len + t (causal; all q_len new tokens are already in
+ *   the cache; reading R25).  A token that sees no key yields o = 0,
+ *   lse = -inf.
+ *   q_len * num_heads <= 256 rows per request (64-row tiles).
+ * Workspace / mla_combine / mla_combine_f32 take num_heads = q_len * num_heads
+ * (rows); out is then [batch, q_len, num_heads, 512].  mla_decode_fp8 is this call
+ * with q_len = 1 (and num_heads <= 128).
+ */
+mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* kv_rope, const float* kv_scale,
+                             const int32_t* block_table, const int32_t* seq_lens, int batch, int num_heads,
+                             int q_len, int kv_lora_rank, int rope_dim, int page_size, int max_pages_per_seq,
+                             int64_t num_pages, float softmax_scale, void* workspace, size_t workspace_bytes,
+                             mla_stream_t stream);
 
 /*
  * mla_combine -- merge split-KV partials left in `workspace` by the preceding

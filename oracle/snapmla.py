@@ -322,6 +322,42 @@ def decode_request(q_rows, pools, block_table_row, L, softmax_scale, **kw):
 
 
 # --------------------------------------------------------------------------
+# NEXT-1: multi-token prediction (MTP).  The paper evaluates query
+# lengths MTP in {1, 2} but does not spell out the mask; reading R25: the q_len new
+# tokens are all in the cache and query token t (0-based) at position L - q_len + t
+# attends causally to keys 0 .. L - q_len + t.
+# --------------------------------------------------------------------------
+def mtp_visible(L, q_len):
+    """Visible key count of each query token: L - (q_len - 1 - t), t = 0..q_len-1 (>= 0)."""
+    return [max(0, int(L) - (q_len - 1 - t)) for t in range(q_len)]
+
+
+def decode_request_mtp(q_tok_rows, pools, block_table_row, L, softmax_scale, **kw):
+    """q_tok_rows [q_len, H, 576]: O7 per query token over its visible keys.
+    Returns o [q_len, H, 512], lse [q_len, H]; a token with no visible key -> 0, -inf."""
+    q_tok_rows = np.asarray(q_tok_rows)
+    T, H = q_tok_rows.shape[0], q_tok_rows.shape[1]
+    o = np.zeros((T, H, D_C))
+    lse = np.full((T, H), -np.inf)
+    for t, Lt in enumerate(mtp_visible(L, T)):
+        if Lt > 0:
+            o[t], lse[t] = decode_request(q_tok_rows[t], pools, block_table_row, Lt, softmax_scale, **kw)
+    return o, lse
+
+
+def attn_o8_mtp(q_tok_rows, c_kv, k_pe, softmax_scale):
+    """O8 (unquantized BF16 MLA, fp64) for q_len query tokens with the causal MTP mask."""
+    q_tok_rows = np.asarray(q_tok_rows, dtype=np.float64)
+    T, H = q_tok_rows.shape[0], q_tok_rows.shape[1]
+    o = np.zeros((T, H, D_C))
+    lse = np.full((T, H), -np.inf)
+    for t, Lt in enumerate(mtp_visible(len(c_kv), T)):
+        if Lt > 0:
+            o[t], lse[t] = attn_o8(q_tok_rows[t], c_kv[:Lt], k_pe[:Lt], softmax_scale)
+    return o, lse
+
+
+# --------------------------------------------------------------------------
 # §4.3 error metrics (P:412): RMSE, cosine difference, relative L2
 # --------------------------------------------------------------------------
 def error_metrics(x, ref):

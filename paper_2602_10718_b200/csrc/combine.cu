@@ -28,9 +28,10 @@ __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ w
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
   float lse = -INFINITY;
   if (c1 > c0) {
-    const int g0 = c0 / per, g1 = (c1 - 1) / per;
+    int g0 = c0 / per, g1 = (c1 - 1) / per;
     float mx = -INFINITY;
     for (int g = g0; g <= g1; ++g) mx = fmaxf(mx, lse_p[((int64_t)(b + g) * n_ht + ht) * kHeadTile + row]);
+    if (mx == -INFINITY) g1 = g0 - 1;   // the row saw no key at all (MTP token beyond a short cache)
     float wsum = 0.f;
     for (int g = g0; g <= g1; ++g) {
       const int64_t pr = ((int64_t)(b + g) * n_ht + ht) * kHeadTile + row;
@@ -46,10 +47,12 @@ __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ w
         acc[4 * i + 3] = fmaf(w, v.w, acc[4 * i + 3]);
       }
     }
-    const float inv = 1.0f / wsum;
+    if (wsum > 0.f) {
+      const float inv = 1.0f / wsum;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] *= inv;
-    lse = mx + logf(wsum);
+      for (int i = 0; i < 16; ++i) acc[i] *= inv;
+      lse = mx + logf(wsum);
+    }
   }
   const int64_t orow = (int64_t)idx * kDc + lane * 16;
   if constexpr (kF32Out) {
@@ -75,7 +78,7 @@ static mla_status launch_combine(const void* workspace, int batch, int num_heads
                                  float* lse, mla_stream_t stream) {
   if (batch < 0 || num_heads <= 0) return MLA_ERR_SHAPE;
   if (kv_lora_rank != kDc) return MLA_ERR_UNSUPPORTED;
-  if (num_heads > 2 * kHeadTile) return MLA_ERR_UNSUPPORTED;
+  if (num_heads > kMaxRows) return MLA_ERR_UNSUPPORTED;
   if (batch == 0) return MLA_OK;
   if (!workspace) return MLA_ERR_WORKSPACE;
   if (!out) return MLA_ERR_NULL;

@@ -82,7 +82,8 @@ struct DecodeParams {
   const int32_t* first_req;
   float* lse_part;
   float* o_part;
-  int batch, num_heads, n_ht, max_pages;
+  int batch, num_heads, n_ht, max_pages;   // num_heads = rows per request = q_len x heads
+  int q_len, heads;                         // MTP: row = t * heads + h for query token t
   float scale_log2;   // softmax_scale * log2(e)
   unsigned long long* trace;   // debug timeline (CTA 0), only in SNAPMLA_TRACE builds
 };
@@ -485,7 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(BAR(q_full));
       }
 
-      const int L = __ldg(p.seq_lens + u.b);
+      // visible keys of this row: query token t = head / heads of q_len sees the cache
+      // up to its own position, L - (q_len - 1 - t) (causal MTP, reading R25)
+      const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
       // S(n) is loaded from TMEM one block ahead: the load of S(n+1) is issued before
       // block n's P' / stats stores, fence and arrive, which hide its latency.
       float tt[32];
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));          // block max of t (local m)
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S2, n);
-        const float mc = mx * c_row;
+        const float mc = mx == -INFINITY ? 0.f : mx * c_row;            // fully masked row block (MTP)
         float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
         float mb0 = 0.f, mb1 = 0.f;
 #pragma unroll
@@ -676,7 +679,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
       }
       // ---------------- epilogue (a9): o = sig_O 2^{m_O - m_ref} O / l ; L = (m_ref + log2 l) ln 2
-      const float f = sig_O * ex2_approx(m_O - m_ref) / l_run;
+      // a row that saw no key in this split (MTP: the split holds only keys after its
+      // query token) leaves o = 0, lse = -inf, which the combine weighs by zero
+      const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;
       const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
       if (row_ok) {
         float* dst = p.o_part + prow * kDc + 256 * w + 128 * hh;
@@ -687,7 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<float4*>(dst + 32 * c + e) =
                 make_float4(o[32 * c + e] * f, o[32 * c + e + 1] * f, o[32 * c + e + 2] * f, o[32 * c + e + 3] * f);
         }
-        if (w == 0 && hh == 0) p.lse_part[prow] = (m_ref + log2f(l_run)) * 0.69314718055994531f;
+        if (w == 0 && hh == 0)
+          p.lse_part[prow] = l_run > 0.f ? (m_ref + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
       }
     }
   }
@@ -761,14 +767,16 @@ extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_s
   return ws_layout(batch, num_heads, num_sms).total;
 }
 
-extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const void* kv_rope,
-                                     const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
-                                     int batch, int num_heads, int kv_lora_rank, int rope_dim, int page_size,
-                                     int max_pages_per_seq, int64_t num_pages, float softmax_scale,
-                                     void* workspace, size_t workspace_bytes, mla_stream_t stream) {
-  if (batch < 0 || num_heads <= 0 || max_pages_per_seq < 0 || num_pages < 0) return MLA_ERR_SHAPE;
+extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* kv_rope,
+                                        const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
+                                        int batch, int num_heads, int q_len, int kv_lora_rank, int rope_dim,
+                                        int page_size, int max_pages_per_seq, int64_t num_pages, float softmax_scale,
+                                        void* workspace, size_t workspace_bytes, mla_stream_t stream) {
+  if (batch < 0 || num_heads <= 0 || q_len <= 0 || max_pages_per_seq < 0 || num_pages < 0) return MLA_ERR_SHAPE;
   if (kv_lora_rank != kDc || rope_dim != kDr || page_size != kPage) return MLA_ERR_UNSUPPORTED;
-  if (num_heads > 2 * kHeadTile) return MLA_ERR_UNSUPPORTED;
+  const int heads = num_heads;
+  if ((int64_t)num_heads * q_len > kMaxRows) return MLA_ERR_UNSUPPORTED;
+  num_heads *= q_len;   // rows per request from here on
   if (num_pages * kPage >= (int64_t)INT32_MAX) return MLA_ERR_UNSUPPORTED;   // TMA row coordinate is int32
   if (!workspace) return MLA_ERR_WORKSPACE;
   if (batch == 0) return MLA_OK;
@@ -814,6 +822,8 @@ extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const
   prm.batch = batch;
   prm.num_heads = num_heads;
   prm.n_ht = n_ht;
+  prm.q_len = q_len;
+  prm.heads = heads;
   prm.max_pages = max_pages_per_seq;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
   prm.trace = g_trace;
@@ -832,4 +842,15 @@ extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, mla_decode_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}
+
+extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const void* kv_rope,
+                                     const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
+                                     int batch, int num_heads, int kv_lora_rank, int rope_dim, int page_size,
+                                     int max_pages_per_seq, int64_t num_pages, float softmax_scale,
+                                     void* workspace, size_t workspace_bytes, mla_stream_t stream) {
+  if (num_heads > 2 * kHeadTile) return MLA_ERR_UNSUPPORTED;
+  return mla_decode_fp8_ex(q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, batch, num_heads, 1, kv_lora_rank,
+                           rope_dim, page_size, max_pages_per_seq, num_pages, softmax_scale, workspace,
+                           workspace_bytes, stream);
 }

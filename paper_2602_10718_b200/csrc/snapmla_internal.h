@@ -15,7 +15,8 @@ constexpr int kDr = 64;       // rope dim
 constexpr int kDqk = kDc + kDr;
 constexpr int kPage = 64;     // tokens per page
 constexpr int kBc = 64;       // key / P-quant block
-constexpr int kHeadTile = 64; // query heads per CTA (UMMA M = 64)
+constexpr int kHeadTile = 64; // query rows per CTA (UMMA M = 64)
+constexpr int kMaxRows = 4 * kHeadTile;   // rows per request (q_len x heads) the decode supports
 constexpr float kSigmaMin = 0x1p-24f;   // reading R2
 
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }

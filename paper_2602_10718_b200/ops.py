@@ -4,7 +4,7 @@ device memory and the current stream; nothing else of torch is used.
 
 Same names as the C ABI (include/snapmla.h):
   mla_kv_append_quant, mla_decode_workspace_bytes, mla_decode_fp8,
-  mla_combine, mla_combine_f32
+  mla_decode_fp8_ex, mla_combine, mla_combine_f32
 There is no CPU fallback: a missing library or a non-CUDA tensor raises.
 """
 import ctypes
@@ -44,6 +44,8 @@ def lib():
     L.mla_decode_workspace_bytes.argtypes = [_I, _I, _I]
     L.mla_decode_fp8.restype = _I
     L.mla_decode_fp8.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
+    L.mla_decode_fp8_ex.restype = _I
+    L.mla_decode_fp8_ex.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
     L.mla_combine.restype = _I
     L.mla_combine.argtypes = [_P, _I, _I, _I, _P, _P, _P]
     L.mla_combine_f32.restype = _I
@@ -54,7 +56,7 @@ def lib():
 
 def exported_symbols():
     return ["mla_status_str", "mla_abi_version", "mla_kv_append_quant", "mla_decode_workspace_bytes",
-            "mla_decode_fp8", "mla_combine", "mla_combine_f32"]
+            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32"]
 
 
 def _check(status, what):
@@ -104,6 +106,19 @@ def mla_decode_fp8(q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, softmax_
         _stream(stream)), "mla_decode_fp8")
 
 
+def mla_decode_fp8_ex(q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, softmax_scale, workspace,
+                      stream=None):
+    """MTP decode: q bf16 [batch, q_len, num_heads, 576]; partials for q_len * num_heads rows."""
+    batch, q_len, num_heads = q.shape[0], q.shape[1], q.shape[2]
+    _check(lib().mla_decode_fp8_ex(
+        _dev(q, torch.bfloat16, "q"), _dev(kv_fp8, torch.uint8, "kv_fp8"),
+        _dev(kv_rope, torch.bfloat16, "kv_rope"), _dev(kv_scale, torch.float32, "kv_scale"),
+        _dev(block_table, torch.int32, "block_table"), _dev(seq_lens, torch.int32, "seq_lens"),
+        batch, num_heads, q_len, D_C, D_R, kv_fp8.shape[1], block_table.shape[1], kv_fp8.shape[0],
+        float(softmax_scale), _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream)), "mla_decode_fp8_ex")
+
+
 def mla_combine(workspace, batch, num_heads, out, lse=None, stream=None):
     """Merge split partials -> out bf16 [batch, num_heads, 512], lse fp32 [batch, num_heads]."""
     _check(lib().mla_combine(
@@ -134,16 +149,23 @@ class PagedMLACache:
 
 def decode_step(q, cache, block_table, seq_lens, softmax_scale, workspace=None, out=None, lse=None,
                 stream=None, f32_out=False):
-    """mla_decode_fp8 + mla_combine.  Returns (out, lse)."""
-    batch, num_heads = q.shape[0], q.shape[1]
+    """mla_decode_fp8 (q [B, H, 576]) or mla_decode_fp8_ex (q [B, q_len, H, 576], MTP) + mla_combine.
+    Returns (out, lse) shaped like q's leading dims."""
+    lead = tuple(q.shape[:-1])
+    batch, rows = q.shape[0], 1
+    for d in lead[1:]:
+        rows *= d
     if workspace is None:
-        workspace = torch.empty(mla_decode_workspace_bytes(batch, num_heads), dtype=torch.uint8, device=q.device)
+        workspace = torch.empty(mla_decode_workspace_bytes(batch, rows), dtype=torch.uint8, device=q.device)
     if out is None:
-        out = torch.empty(batch, num_heads, D_C, dtype=torch.float32 if f32_out else torch.bfloat16,
-                          device=q.device)
+        out = torch.empty(lead + (D_C,), dtype=torch.float32 if f32_out else torch.bfloat16, device=q.device)
     if lse is None:
-        lse = torch.empty(batch, num_heads, dtype=torch.float32, device=q.device)
-    mla_decode_fp8(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,
-                   workspace, stream)
-    (mla_combine_f32 if f32_out else mla_combine)(workspace, batch, num_heads, out, lse, stream)
+        lse = torch.empty(lead, dtype=torch.float32, device=q.device)
+    if q.dim() == 4:
+        mla_decode_fp8_ex(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,
+                          workspace, stream)
+    else:
+        mla_decode_fp8(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,
+                       workspace, stream)
+    (mla_combine_f32 if f32_out else mla_combine)(workspace, batch, rows, out, lse, stream)
     return out, lse

@@ -16,16 +16,19 @@ PAGE = 64
 class Case:
     """B requests with lengths `lens`, H heads, random page permutation."""
 
-    def __init__(self, lens, H, seed=0, dist="mla", extra_pages=3, softmax_scale=None):
+    def __init__(self, lens, H, seed=0, dist="mla", extra_pages=3, softmax_scale=None, q_len=1):
         self.lens = np.asarray(lens, dtype=np.int64)
-        self.B, self.H = len(lens), H
+        self.B, self.H, self.q_len = len(lens), H, q_len
         self.scale = synth.DEFAULT_SOFTMAX_SCALE if softmax_scale is None else softmax_scale
         rng = np.random.default_rng(seed)
         self.bt, self.num_pages = synth.paged_layout(rng, self.lens, extra_pages=extra_pages)
         n_tok = int(self.lens.sum())
         c, r = synth.latent_tokens(rng, max(n_tok, 1), dist)
         self.c_kv, self.k_pe = c[:n_tok], r[:n_tok]              # bf16 CPU tensors
-        self.q = synth.queries(rng, self.B * H, dist).reshape(self.B, H, 576)
+        if q_len == 1:
+            self.q = synth.queries(rng, self.B * H, dist).reshape(self.B, H, 576)
+        else:   # MTP: q [B, q_len, H, 576]
+            self.q = synth.queries(rng, self.B * q_len * H, dist).reshape(self.B, q_len, H, 576)
         # flattened token -> (request, position) and its paged slot
         self.tok_req = np.repeat(np.arange(self.B), self.lens)
         self.tok_pos = np.concatenate([np.arange(L) for L in self.lens]) if n_tok else np.zeros(0, np.int64)
@@ -68,6 +71,10 @@ class Case:
             pools["kv_rope"].reshape(-1, 64)[slots] = rope
             pools["kv_scale"].reshape(-1)[slots] = sig
         return pools
+
+    def oracle_request_mtp(self, pools, b):
+        """O7 per query token over its causally visible keys (reading R25)."""
+        return O.decode_request_mtp(self.q[b].float().numpy(), pools, self.bt[b], int(self.lens[b]), self.scale)
 
     def oracle_request(self, pools, b, heads=None, which="o7"):
         L = int(self.lens[b])

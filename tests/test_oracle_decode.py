@@ -200,3 +200,55 @@ def test_error_metrics_definitions():
     assert m["rel_l2"] == pytest.approx(1.0)
     assert m["cos_diff"] == pytest.approx(0.0, abs=1e-15)
     assert m["rmse"] == pytest.approx(np.sqrt((9 + 16) / 2))
+
+
+# ---- MTP (NEXT-1, reading R25): the causal mask convention pinned against torch SDPA
+@pytest.mark.parametrize("L,T", [(5, 2), (64, 2), (130, 3), (1, 2)])
+def test_o8_mtp_vs_torch_masked_sdpa(L, T):
+    rng = np.random.default_rng(31 + L)
+    H = 3
+    c = rng.normal(size=(L, 512))
+    r = rng.normal(size=(L, 64))
+    q = rng.normal(size=(T, H, 576))
+    o, lse = O.attn_o8_mtp(q, c, r, SCALE)
+    k = torch.from_numpy(np.concatenate([c, r], 1))
+    v = torch.from_numpy(c)
+    qt = torch.from_numpy(q.reshape(T * H, 576))
+    tok = np.repeat(np.arange(T), H)
+    visible = torch.from_numpy(np.arange(L)[None, :] <= (L - T + tok)[:, None])   # key j visible to row
+    for row in range(T * H):
+        t, h = divmod(row, H)
+        if not visible[row].any():
+            assert np.all(o[t, h] == 0) and lse[t, h] == -np.inf
+            continue
+        o_ref = F.scaled_dot_product_attention(qt[row][None, None, None], k[None, None], v[None, None],
+                                               attn_mask=visible[row][None, None, None], scale=SCALE)[0, 0, 0]
+        s = SCALE * (qt[row] @ k.T)
+        lse_ref = torch.logsumexp(s[visible[row]], dim=0)
+        np.testing.assert_allclose(o[t, h], o_ref.numpy(), rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(lse[t, h], lse_ref.item(), rtol=1e-12)
+
+
+def _pools_for(d):
+    """the case's tokens in a fresh paged pool (identity page order)."""
+    L = len(d["c"])
+    npages = (L + 63) // 64
+    pools = dict(kv_fp8=np.zeros((npages, 64, 512), np.uint8), kv_rope=np.zeros((npages, 64, 64), np.uint16),
+                 kv_scale=np.zeros((npages, 64), np.float32))
+    slots = np.arange(L)
+    pools["kv_fp8"].reshape(-1, 512)[slots] = d["kc"]
+    pools["kv_rope"].reshape(-1, 64)[slots] = d["kr"]
+    pools["kv_scale"].reshape(-1)[slots] = d["sk"]
+    return pools, np.arange(npages)
+
+
+def test_mtp_last_token_is_single_token_decode():
+    d = _case(200, seed=41)
+    pools, bt = _pools_for(d)
+    q2 = np.stack([d["q"], d["q"][::-1].copy()])               # [2, H, 576]
+    o2, l2 = O.decode_request_mtp(q2, pools, bt, 200, SCALE)
+    o1, l1 = O.decode_request(q2[1], pools, bt, 200, SCALE)
+    o0, l0 = O.decode_request(q2[0], pools, bt, 199, SCALE)
+    np.testing.assert_array_equal(o2[1], o1)
+    np.testing.assert_array_equal(o2[0], o0)
+    np.testing.assert_array_equal(l2[0], l0)
