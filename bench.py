@@ -12,6 +12,8 @@ collective) -> "scaling": "weak"; value = tokens of all ranks / max-rank time.
 all-gathers the output over NCCL.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py --mtp 2            # NEXT-1: q_len = 2 query tokens per request
+  python bench.py --sweep            # BASELINE.json configs[4]: DeepSeek-R1 shape, context x batch grid
 """
 import argparse
 import json
@@ -53,6 +55,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs: no clock-settle loop, no e2e leg, no cpu baseline")
+    ap.add_argument("--mtp", type=int, default=1, help="query tokens per request per step (MTP, NEXT-1)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE.json configs[4]: DeepSeek-R1 shape over contexts 4K-128K x batch 1-512")
     return ap.parse_args()
 
 
@@ -141,6 +146,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     w = workload(args)
     B, H, L = w["batch"], w["heads"], w["context"]
+    T = args.mtp
     head0, head1 = D.tp_range(H, world, rank) if args.mode == "tp" else (0, H)
     heads_local = head1 - head0
     scale = synth.DEFAULT_SOFTMAX_SCALE
@@ -164,13 +170,21 @@ def run_ours(args, rank, world, local_rank):
         sl_v = (pos % 64 + 1).to(torch.int32)
         c, r = synth.torch_latent(idx.numel(), gen, dev)
         cache.append(c, r, bt_v, sl_v)
-    q_all = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
-    q = q_all[:, head0:head1].contiguous()
-    new_c, new_r = synth.torch_latent(B, gen, dev)
+    if T == 1:
+        q_all = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
+        q = q_all[:, head0:head1].contiguous()
+    else:   # MTP: q [B, T, heads, 576]
+        q_all = synth.torch_queries(B * T * H, gen, dev).view(B, T, H, 576)
+        q = q_all[:, :, head0:head1].contiguous()
+    rows = T * heads_local
+    new_cr = [synth.torch_latent(B, gen, dev) for _ in range(T)]   # the T new tokens of every request
+    new_c, new_r = new_cr[-1]
     seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
-    ws = torch.empty(ops.mla_decode_workspace_bytes(B, heads_local), dtype=torch.uint8, device=dev)
-    out = torch.empty(B, heads_local, 512, dtype=torch.bfloat16, device=dev)
-    lse = torch.empty(B, heads_local, dtype=torch.float32, device=dev)
+    seq_lens_t = [torch.full((B,), L - (T - 1 - t), dtype=torch.int32, device=dev) for t in range(T)]
+    ws = torch.empty(ops.mla_decode_workspace_bytes(B, rows), dtype=torch.uint8, device=dev)
+    out = torch.empty((B, T, heads_local, 512) if T > 1 else (B, heads_local, 512), dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(out.shape[:-1], dtype=torch.float32, device=dev)
+    decode = ops.mla_decode_fp8_ex if T > 1 else ops.mla_decode_fp8
     gathered = torch.empty(world, B, heads_local, 512, dtype=torch.bfloat16, device=dev) if args.mode == "tp" else None
     del q_all
     torch.cuda.synchronize()
@@ -180,14 +194,15 @@ def run_ours(args, rank, world, local_rank):
     ev_d1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
     def step(i=None):
-        # a1: the new token of every request lands at position L-1 (same slot each step)
-        cache.append(new_c, new_r, block_table, seq_lens)
+        # a1: the T new tokens of every request land at positions L-T .. L-1 (same slots each step)
+        for t in range(T):
+            cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         if i is not None:
             ev_d0[i].record(stream)
-        ops.mla_decode_fp8(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        decode(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
         if i is not None:
             ev_d1[i].record(stream)
-        ops.mla_combine(ws, B, heads_local, out, lse)
+        ops.mla_combine(ws, B, rows, out, lse)
         if gathered is not None:
             D.tp_gather_heads(out, gathered=gathered)
 
@@ -222,9 +237,16 @@ def run_ours(args, rank, world, local_rank):
         ms, dec_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
 
+    peak, peak_src = measured_peaks()
+    kv_bytes = B * L * BYTES_PER_TOKEN
+    dec_bytes = kv_bytes + B * rows * 576 * 2       # algorithmic bytes per decode launch
+    achieved = dec_bytes / (dec_ms / 1e3) / 1e9
+    tokens_per_step = B * T * (world if args.mode == "dp" else 1)
     if args.quick:
-        return {"metric": METRIC, "value": round(B * (world if args.mode == "dp" else 1) / (ms_step / 1e3), 1),
-                "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True}
+        return {"metric": METRIC, "value": round(tokens_per_step / (ms_step / 1e3), 1),
+                "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True,
+                "batch": B, "heads": H, "context": L, "mtp": T,
+                "roofline_frac": round(achieved / peak, 4), "achieved_gbs": round(achieved, 1), "clocks": clk}
 
     # ---------------- e2e: host buffers through the public API
     q_h = q.cpu().pin_memory()
@@ -237,9 +259,11 @@ def run_ours(args, rank, world, local_rank):
         q_d.copy_(q_h, non_blocking=True)
         c_d.copy_(c_h, non_blocking=True)
         r_d.copy_(r_h, non_blocking=True)
+        for t in range(T - 1):
+            cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         cache.append(c_d, r_d, block_table, seq_lens)
-        ops.mla_decode_fp8(q_d, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
-        ops.mla_combine(ws, B, heads_local, out, lse)
+        decode(q_d, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        ops.mla_combine(ws, B, rows, out, lse)
         if gathered is not None:
             D.tp_gather_heads(out, gathered=gathered)
         out_h.copy_(out, non_blocking=True)
@@ -265,13 +289,8 @@ def run_ours(args, rank, world, local_rank):
     h2d = q_h.numel() * 2 + c_h.numel() * 2 + r_h.numel() * 2
     d2h = out_h.numel() * 2 + lse_h.numel() * 4
 
-    tokens_per_step = B * (world if args.mode == "dp" else 1)
     value = tokens_per_step / (ms_step / 1e3)
-    peak, peak_src = measured_peaks()
-    kv_bytes = B * L * BYTES_PER_TOKEN
-    dec_bytes = kv_bytes + B * heads_local * 576 * 2       # algorithmic bytes per decode launch
-    achieved = dec_bytes / (dec_ms / 1e3) / 1e9
-    launches_per_step = 4   # append, plan, decode, combine (all ours)
+    launches_per_step = T + 3   # append x T, plan, decode, combine (all ours)
     res = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -287,16 +306,16 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
         "config": {
             "workload": w["name"], "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
-            "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": 1,
+            "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": T,
             "parallelism": f"{args.mode}{world}",
             "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
         },
         "roofline": {
             "bound": "hbm", "kernel": "mla_decode_fp8 (plan + decode launches)",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
+            "traffic": ncu_traffic(args.workload) if T == 1 else None, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": dec_bytes, "decode_ms": round(dec_ms, 4),
-            "bytes_per_unit": f"{BYTES_PER_TOKEN} B per cached token + 1152 B per (request, head) q row",
+            "bytes_per_unit": f"{BYTES_PER_TOKEN} B per cached token + 1152 B per (request, query token, head) q row",
         },
         "e2e": {"value": round(tokens_per_step / (e_ms / args.steps / 1e3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -392,6 +411,32 @@ def run_reference(args):
     }
 
 
+SWEEP_CONTEXTS = (4096, 8192, 16384, 32768, 65536, 131072)
+SWEEP_BATCHES = (1, 8, 64, 512)
+
+
+def run_sweep(args, rank, world, local_rank):
+    """BASELINE.json configs[4]: DeepSeek-R1 shape (128 heads) over context x batch,
+    append + decode + combine per step; one JSON line with every point (per rank;
+    DP ranks run the same grid on their own requests)."""
+    import torch
+    pts = []
+    for L in SWEEP_CONTEXTS:
+        for B in SWEEP_BATCHES:
+            if B * L * BYTES_PER_TOKEN > 60e9:   # keep the pool well inside HBM
+                continue
+            a = argparse.Namespace(**vars(args))
+            a.workload, a.batch, a.context, a.heads, a.quick = "dsr1", B, L, 128, True
+            a.steps, a.warmup = max(5, min(args.steps, 20)), 3
+            r = run_ours(a, rank, world, local_rank)
+            pts.append({k: r[k] for k in ("batch", "context", "value", "ms_per_step", "decode_ms",
+                                          "roofline_frac", "achieved_gbs")} | {"sm_mhz": r["clocks"]["sm_mhz"]})
+            torch.cuda.empty_cache()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "sweep": "BASELINE.json configs[4] (DeepSeek-R1 shape, 128 heads)",
+                          "unit": "tokens/s", "n_gpus": world, "points": pts}))
+
+
 def main():
     args = parse()
     rank, world, local_rank = dist_env()
@@ -404,6 +449,9 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.sweep:
+        run_sweep(args, rank, world, local_rank)
+        return
     res = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         res["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
