@@ -14,6 +14,7 @@ all-gathers the output over NCCL.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
   python bench.py --mtp 2            # NEXT-1: q_len = 2 query tokens per request
   python bench.py --sweep            # BASELINE.json configs[4]: DeepSeek-R1 shape, context x batch grid
+  python bench.py --fetch            # NEXT-3: Fused-Fetch-Dequant of the whole workload cache (GB/s)
 """
 import argparse
 import json
@@ -56,6 +57,7 @@ def parse():
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs: no clock-settle loop, no e2e leg, no cpu baseline")
     ap.add_argument("--mtp", type=int, default=1, help="query tokens per request per step (MTP, NEXT-1)")
+    ap.add_argument("--fetch", action="store_true", help="time mla_kv_fetch_dequant over the workload cache")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE.json configs[4]: DeepSeek-R1 shape over contexts 4K-128K x batch 1-512")
     return ap.parse_args()
@@ -411,6 +413,55 @@ def run_reference(args):
     }
 
 
+def run_fetch(args, local_rank):
+    """NEXT-3: Fused-Fetch-Dequant of every cached token of the workload (one launch
+    per step); HBM-bound: 644 B read + 1152 B written per token."""
+    import torch
+    from paper_2602_10718_b200 import ops, synth
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workload(args)
+    B, L = w["batch"], w["context"]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99)
+    ppr = (L + 63) // 64
+    cache = ops.PagedMLACache(B * ppr, dev)
+    bt = torch.randperm(B * ppr, generator=gen, device=dev).to(torch.int32).view(B, ppr).contiguous()
+    for s0 in range(0, B * L, 1 << 18):
+        idx = torch.arange(s0, min(s0 + (1 << 18), B * L), device=dev)
+        req, pos = idx // L, idx % L
+        c, r = synth.torch_latent(idx.numel(), gen, dev)
+        cache.append(c, r, bt[req, pos // 64].view(-1, 1).contiguous(), (pos % 64 + 1).to(torch.int32))
+    starts = torch.zeros(B, dtype=torch.int32, device=dev)
+    offs = (torch.arange(B, device=dev, dtype=torch.int32) * L).contiguous()
+    total = B * L
+    c_out = torch.empty(total, 512, dtype=torch.bfloat16, device=dev)
+    r_out = torch.empty(total, 64, dtype=torch.bfloat16, device=dev)
+
+    def one():
+        ops.mla_kv_fetch_dequant(cache.kv_fp8, cache.kv_rope, cache.kv_scale, bt, starts, offs, total, c_out, r_out)
+
+    for _ in range(max(3, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    nbytes = total * (BYTES_PER_TOKEN + 1152)
+    peak, peak_src = measured_peaks()
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"metric": "Fused-Fetch-Dequant tokens/s (NEXT-3)", "value": round(total / (ms / 1e3), 1),
+            "unit": "tokens/s", "ms_per_step": round(ms, 4), "steps": args.steps, "warmup": args.warmup,
+            "config": {"workload": w["name"], "tokens": total},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "peak_source": peak_src,
+                         "bytes_per_unit": "644 B read + 1152 B written per token"}}
+
+
 SWEEP_CONTEXTS = (4096, 8192, 16384, 32768, 65536, 131072)
 SWEEP_BATCHES = (1, 8, 64, 512)
 
@@ -451,6 +502,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.sweep:
         run_sweep(args, rank, world, local_rank)
+        return
+    if args.fetch:
+        if rank == 0:
+            print(json.dumps(run_fetch(args, local_rank)))
         return
     res = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:

@@ -10,6 +10,7 @@
  *                        Appendix C order enforcement P:759-764); Q quantization
  *                        (Fused-Q-Quant) runs in its prologue
  *   mla_decode_fp8_ex    the same with q_len query tokens per request (MTP)
+ *   mla_kv_fetch_dequant Fused-Fetch-Dequant (§3.3): paged FP8 cache -> BF16
  *   mla_combine          split-KV merge of the per-split (o, logsumexp) partials
  *                        (Algorithm 1 returns o and L)
  *
@@ -149,6 +150,25 @@ mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* k
  */
 mla_status mla_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out, float* lse,
                        mla_stream_t stream);
+
+/*
+ * mla_kv_fetch_dequant -- Fused-Fetch-Dequant (§3.3; NEXT-3): read the
+ * cached tokens [tok_start[b], tok_start[b] + count_b) of every request from the
+ * paged pools and dequantize them on load:
+ *   c_kv_out[i, d] = BF16(fp32(dec(code) * sigma_K))        d < 512
+ *   k_pe_out[i, e] = BF16(fp32(k_r'[e] * sigma_K))          e < 64 (undoes Eq.6)
+ * (one fp32 RNE product, then RNE to BF16; reading R26).
+ *   out_offset   int32 [batch] exclusive prefix of the per-request counts: request
+ *                b's tokens are output rows out_offset[b] .. out_offset[b] + count_b - 1,
+ *                rows in token order; total_rows = sum of counts.  Ranges must lie
+ *                inside each request's cache (not checked on the device).
+ *   c_kv_out     bf16 [total_rows, 512];  k_pe_out bf16 [total_rows, 64]
+ */
+mla_status mla_kv_fetch_dequant(const uint8_t* kv_fp8, const void* kv_rope, const float* kv_scale,
+                                const int32_t* block_table, const int32_t* tok_start, const int32_t* out_offset,
+                                int batch, int kv_lora_rank, int rope_dim, int page_size, int max_pages_per_seq,
+                                int64_t num_pages, int64_t total_rows, void* c_kv_out, void* k_pe_out,
+                                mla_stream_t stream);
 
 /* Same as mla_combine but writes fp32 output [batch, num_heads, kv_lora_rank]
  * (diagnostic: exposes the kernel result before the final BF16 rounding). */

@@ -358,6 +358,24 @@ def attn_o8_mtp(q_tok_rows, c_kv, k_pe, softmax_scale):
 
 
 # --------------------------------------------------------------------------
+# NEXT-3: Fused-Fetch-Dequant (§3.3).  SPEC: C[i] = fp8_decode(code_i)
+# * scale_i; K_r[i] = rope_i * scale_i (undoing the domain alignment); rows in
+# token order.  Reading R26 (the paper names no output precision; the cache
+# inputs were BF16): one fp32 product (IEEE RNE), then RNE to BF16.
+# --------------------------------------------------------------------------
+def fetch_dequant(pools, block_table_row, start, count):
+    """Tokens start .. start+count-1 of one request -> (c_kv bf16 bits [count,512],
+    k_pe bf16 bits [count,64])."""
+    slots = np.array([slot_of(block_table_row, start + i) for i in range(count)], dtype=np.int64)
+    codes = pools["kv_fp8"].reshape(-1, D_C)[slots]
+    rope = pools["kv_rope"].reshape(-1, D_R)[slots]
+    sig = pools["kv_scale"].reshape(-1)[slots].astype(np.float32)
+    c = decode_e4m3(codes).astype(np.float32) * sig[:, None]                       # fp32 RNE product
+    r = bf16_bits_to_f64(rope).astype(np.float32) * sig[:, None]
+    return bf16_rne_bits(c), bf16_rne_bits(r)
+
+
+# --------------------------------------------------------------------------
 # §4.3 error metrics (P:412): RMSE, cosine difference, relative L2
 # --------------------------------------------------------------------------
 def error_metrics(x, ref):

@@ -4,7 +4,7 @@ device memory and the current stream; nothing else of torch is used.
 
 Same names as the C ABI (include/snapmla.h):
   mla_kv_append_quant, mla_decode_workspace_bytes, mla_decode_fp8,
-  mla_decode_fp8_ex, mla_combine, mla_combine_f32
+  mla_decode_fp8_ex, mla_combine, mla_combine_f32, mla_kv_fetch_dequant
 There is no CPU fallback: a missing library or a non-CUDA tensor raises.
 """
 import ctypes
@@ -46,6 +46,8 @@ def lib():
     L.mla_decode_fp8.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
     L.mla_decode_fp8_ex.restype = _I
     L.mla_decode_fp8_ex.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
+    L.mla_kv_fetch_dequant.restype = _I
+    L.mla_kv_fetch_dequant.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _I64, _P, _P, _P]
     L.mla_combine.restype = _I
     L.mla_combine.argtypes = [_P, _I, _I, _I, _P, _P, _P]
     L.mla_combine_f32.restype = _I
@@ -56,7 +58,7 @@ def lib():
 
 def exported_symbols():
     return ["mla_status_str", "mla_abi_version", "mla_kv_append_quant", "mla_decode_workspace_bytes",
-            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32"]
+            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant"]
 
 
 def _check(status, what):
@@ -130,6 +132,24 @@ def mla_combine_f32(workspace, batch, num_heads, out, lse=None, stream=None):
     _check(lib().mla_combine_f32(
         _dev(workspace, torch.uint8, "workspace"), batch, num_heads, D_C, _dev(out, torch.float32, "out"),
         None if lse is None else _dev(lse, torch.float32, "lse"), _stream(stream)), "mla_combine_f32")
+
+
+def mla_kv_fetch_dequant(kv_fp8, kv_rope, kv_scale, block_table, tok_start, out_offset, total_rows,
+                         c_kv_out=None, k_pe_out=None, stream=None):
+    """Fused-Fetch-Dequant: rows of the paged FP8 cache -> BF16 (c_kv [total, 512], k_pe [total, 64])."""
+    dev = kv_fp8.device
+    if c_kv_out is None:
+        c_kv_out = torch.empty(total_rows, D_C, dtype=torch.bfloat16, device=dev)
+    if k_pe_out is None:
+        k_pe_out = torch.empty(total_rows, D_R, dtype=torch.bfloat16, device=dev)
+    _check(lib().mla_kv_fetch_dequant(
+        _dev(kv_fp8, torch.uint8, "kv_fp8"), _dev(kv_rope, torch.bfloat16, "kv_rope"),
+        _dev(kv_scale, torch.float32, "kv_scale"), _dev(block_table, torch.int32, "block_table"),
+        _dev(tok_start, torch.int32, "tok_start"), _dev(out_offset, torch.int32, "out_offset"),
+        tok_start.shape[0], D_C, D_R, kv_fp8.shape[1], block_table.shape[1], kv_fp8.shape[0], int(total_rows),
+        _dev(c_kv_out, torch.bfloat16, "c_kv_out"), _dev(k_pe_out, torch.bfloat16, "k_pe_out"),
+        _stream(stream)), "mla_kv_fetch_dequant")
+    return c_kv_out, k_pe_out
 
 
 class PagedMLACache:
