@@ -376,6 +376,57 @@ def fetch_dequant(pools, block_table_row, start, count):
 
 
 # --------------------------------------------------------------------------
+# NEXT-4(a): Table 2 KV-cache quantization configurations (granularities
+# of Appendix A), for the numerical-accuracy ablation.  Each returns the
+# DEQUANTIZED cache (content [L,512], rope [L,64]) in fp64; E4M3 RNE/satfinite codec
+# throughout; dynamic scales sigma = max(amax / 448, 2^-24) (R1, R2).
+# --------------------------------------------------------------------------
+def _deq(x, sigma):
+    return decode_e4m3(encode_e4m3(np.asarray(x, np.float64) / sigma)) * sigma
+
+
+def kv_quant_config(content, rope, config, block=64):
+    """config: "snapmla" (per-token content, RoPE BF16 pre-scaled, Eq.6), "A" (per-token
+    over the whole 576-d row, RoPE quantized too), "B" (per-tensor static scale 1.0,
+    RoPE unquantized), "C" (per-tensor dynamic, RoPE unquantized), "D" (per-block
+    block x block tiles of the content, RoPE unquantized)."""
+    c = np.asarray(content, np.float64)
+    r = np.asarray(rope, np.float64)
+    if config == "snapmla":
+        codes, sig, rbits = per_token_quant(c.astype(np.float32), r.astype(np.float32))
+        s = sig.astype(np.float64)[:, None]
+        return decode_e4m3(codes) * s, bf16_bits_to_f64(rbits) * s
+    if config == "A":
+        row = np.concatenate([c, r], axis=1)
+        sig = np.maximum(np.abs(row).max(axis=1, keepdims=True) / E4M3_MAX, 2.0 ** -24)
+        q = _deq(row, sig)
+        return q[:, :D_C], q[:, D_C:]
+    if config == "B":
+        return _deq(c, 1.0), r
+    if config == "C":
+        return _deq(c, max(np.abs(c).max() / E4M3_MAX, 2.0 ** -24)), r
+    if config == "D":
+        out = np.empty_like(c)
+        for i in range(0, c.shape[0], block):
+            for j in range(0, c.shape[1], block):
+                blk = c[i:i + block, j:j + block]
+                out[i:i + block, j:j + block] = _deq(blk, max(np.abs(blk).max() / E4M3_MAX, 2.0 ** -24))
+        return out, r
+    raise ValueError(config)
+
+
+def attn_dequantized(q, c_deq, r_deq, softmax_scale):
+    """exact fp64 softmax attention (Eq.5) of unquantized queries over a dequantized cache,
+    V = the dequantized content (the KV-only part of the ablation)."""
+    q = np.asarray(q, np.float64)
+    s = float(softmax_scale) * (q[:, :D_C] @ c_deq.T + q[:, D_C:] @ r_deq.T)
+    m = s.max(axis=1)
+    e = np.exp(s - m[:, None])
+    den = e.sum(axis=1)
+    return (e @ c_deq) / den[:, None], m + np.log(den)
+
+
+# --------------------------------------------------------------------------
 # §4.3 error metrics (P:412): RMSE, cosine difference, relative L2
 # --------------------------------------------------------------------------
 def error_metrics(x, ref):
