@@ -42,16 +42,14 @@
 namespace snapmla {
 
 constexpr int kThreads = 512;     // 16 warps
-#ifndef SNAPMLA_ACC_TOP
-#define SNAPMLA_ACC_TOP 1
-#endif
-// the SM schedulers prefer the highest eligible warp id: the accumulators (issue-starved
-// otherwise) take the top ids
-constexpr int kWarpAcc = SNAPMLA_ACC_TOP ? 8 : 0;   // +0-3 accumulators, O cols 0-255; +4-7 cols 256-511
-constexpr int kWarpSm = SNAPMLA_ACC_TOP ? 0 : 8;    // +0-3 softmax set 0 (even blocks; owns TMEM), +4-7 set 1
+constexpr int kWarpAcc = 0;       // 0-3 accumulators, O cols 0-255; 4-7 cols 256-511
+constexpr int kWarpTma = 8;       // 8     TMA producer
+constexpr int kWarpQk = 9;        // 9     QK issuer, owns TMEM
+constexpr int kWarpPv = 10;       // 10-11 PV_L / PV_R issuers
+constexpr int kWarpSoftmax = 12;  // 12-15 softmax
 // register budget (setmaxnreg; balanced per SMSP: 2 acc + 1 issue + 1 softmax warp each):
 // 256 x 176 + 128 x 40 + 128 x 120 = 65,536 = 512 x 128 (launch)
-constexpr uint32_t kRegsAcc = 168, kRegsSm = 88;
+constexpr uint32_t kRegsAcc = 176, kRegsIssue = 40, kRegsSoftmax = 120;
 constexpr int kSlots = 5;         // KV ring depth (blocks)
 constexpr int kPSlots = 2;        // P' + stats ring depth (blocks)
 constexpr int kSSlots = 2;        // S ring depth (TMEM)
@@ -66,7 +64,7 @@ constexpr uint32_t kOffScaleHi = 5 * 8192 + 144;            // sigma_K of tokens
 constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
 constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-static_assert(2 * 32 * kRegsAcc + 2 * 32 * kRegsSm <= 4 * 32 * 128,
+static_assert(2 * 32 * kRegsAcc + 32 * kRegsIssue + 32 * kRegsSoftmax <= 4 * 32 * 128,
               "setmaxnreg budget per SMSP (launch: 4 warps x 128 registers)");
 
 // instruction descriptors (M = 64)
@@ -106,7 +104,7 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
 #endif
 
 struct Bars {
-  uint64_t kv_full[kSlots];                     // TMA -> QK (slot reuse follows PV completion)
+  uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
   uint64_t s_full[kSSlots], s_empty[kSSlots];   // QK -> softmax / softmax -> QK
   uint64_t p_full[kPSlots], p_empty[kPSlots];   // P' + stats: softmax -> PV, acc / PV_L + PV_R + acc -> softmax
   uint64_t t_full[kTSlots], t_free[kTSlots];    // T ring: PV -> WG / WG -> PV
@@ -284,76 +282,6 @@ __device__ __forceinline__ uint32_t t_slot_addr(uint32_t tmem, uint32_t s) {
   return tmem + (s == 0 ? 256u : (16u << 16) + 256u * (s - 1));
 }
 
-// QK(m) into S slot m % 2: waits its KV slot and the S slot, one elected issue of the
-// 20 MMAs + commit (whole warp, converged).
-__device__ __forceinline__ void qk_block(uint32_t m, uint32_t sbase, uint32_t bar0, uint32_t tmem, uint64_t dQr) {
-  const uint32_t st = m % kSlots, ss = m % kSSlots;
-  mbar_wait(BAR(kv_full) + 8 * st, (m / kSlots) & 1, 3, m);
-  mbar_wait(BAR(s_empty) + 8 * ss, ((m / kSSlots) & 1) ^ 1, 4, m);
-  tc_fence_after();
-  const uint32_t kv = sbase + kOffKv + st * kStage;
-  qk_issue(tmem + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
-           make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
-}
-
-// PV of one block, both 256-column halves (T slots tl / tr), one commit group:
-// t_full of both slots and p_empty (so t_full of either half implies the whole PV(n)).
-__device__ __forceinline__ void pv_issue2(uint32_t dTl, uint32_t dTr, uint64_t dP, uint64_t dVl, uint64_t dVr,
-                                          uint32_t bar_tl, uint32_t bar_tr, uint32_t bar_p) {
-  asm volatile(
-      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
-      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "add.s64 a, %2, 128;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %2, %3, %5, pf;\n\t"
-      "add.s64 b, %3, 256;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %5, pt;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%1], %2, %4, %5, pf;\n\t"
-      "add.s64 b, %4, 256;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%1], a, b, %5, pt;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}"
-      ::"r"(dTl), "r"(dTr), "l"(dP), "l"(dVl), "l"(dVr), "r"(kIdescPv), "r"(bar_tl), "r"(bar_tr), "r"(bar_p)
-      : "memory");
-}
-
-// The TMA producer's own walk over the CTA's (request, block) sequence.
-struct ProdIter {
-  UnitIter it;
-  Unit u;
-  int j;
-  bool have;
-  __device__ bool next(int& b, int& jj) {
-    while (true) {
-      if (have && j < u.k1) {
-        b = u.b;
-        jj = j++;
-        return true;
-      }
-      if (!it.next(u)) return false;
-      have = true;
-      j = u.k0;
-    }
-  }
-};
-
-// one key block (request b, block j) into KV slot `slot`: 4 x 8 KB FP8 boxes + 8 KB
-// BF16 RoPE box (SWIZZLE_128B, row from the block table) + the two scale halves
-__device__ __forceinline__ void load_block(uint32_t slot, int b, int j, const DecodeParams& p, uint32_t sbase,
-                                           uint32_t bar0, const CUtensorMap* tm_kv, const CUtensorMap* tm_rope,
-                                           uint64_t pol) {
-  const int row = __ldg(p.block_table + (int64_t)b * p.max_pages + j) * kPage;
-  const uint32_t dst = sbase + kOffKv + slot * kStage;
-  const uint32_t full = BAR(kv_full) + 8 * slot;
-  mbar_arrive_expect_tx(full, kKvTx);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, tm_kv, full, c * 128, row, pol);
-  tma_load_2d(dst + 4 * kBoxBytes, tm_rope, full, 0, row, pol);
-  bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 128, full, pol);
-  bulk_load(dst + kOffScaleHi, p.kv_scale + (int64_t)row + 32, 128, full, pol);
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
                       const DecodeParams p) {
@@ -366,10 +294,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(BAR(kv_full) + 8 * i, 1);
+      mbar_init(BAR(kv_empty) + 8 * i, 2);
     }
     for (int i = 0; i < kPSlots; ++i) {
-      mbar_init(BAR(p_full) + 8 * i, 1);        // the softmax set, after its named barrier
-      mbar_init(BAR(p_empty) + 8 * i, 1 + 8);   // the PV commit group, 8 accumulator warps (stats read)
+      mbar_init(BAR(p_full) + 8 * i, 4);
+      mbar_init(BAR(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(BAR(s_full) + 8 * i, 1);
@@ -379,11 +308,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(BAR(t_full) + 8 * i, 1);
       mbar_init(BAR(t_free) + 8 * i, 4);
     }
-    mbar_init(BAR(q_full), 1);                  // set 0 wrote Q
-    mbar_init(BAR(q_free), 2);                  // both QK-issuing warps' commits per unit
+    mbar_init(BAR(q_full), 4);
+    mbar_init(BAR(q_free), 1);
     fence_barrier_init();
   }
-  if (warp == kWarpSm) tmem_alloc(BAR(tmem_base), 512);
+  if (warp == kWarpTma && lane == 0) {
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_rope);
+  }
+  if (warp == kWarpQk) tmem_alloc(BAR(tmem_base), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -408,15 +341,74 @@ __global__ void __launch_bounds__(kThreads, 1)
   UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
   Unit u;
 
-  if (warp >= kWarpSm && warp < kWarpSm + 8) {
-    if constexpr (kRegsSm > 128) regs_inc<kRegsSm>();   // launch: 128 per thread
-    else regs_dec<kRegsSm>();
-    // ===== softmax set s (warps 8-11: even blocks, 12-15: odd blocks — Alg.1's WG0 / WG1
-    // alternation): thread = (row, 32-token half).  The set that handles block n
-    // also issues QK(n+2) into the S slot it just freed (warp k = 0) and PV(n) once its
-    // P'(n) is stored (warp k = 1): no dedicated issue warps, so the register file holds
-    // two softmax warps per SMSP next to the register-resident O.
-    const int set = (warp - kWarpSm) >> 2;
+  if (warp >= kWarpTma && warp < kWarpSoftmax) {
+    regs_dec<kRegsIssue>();
+    if (warp == kWarpTma) {
+      // ============================ TMA producer ============================
+      if (lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        uint32_t n = 0;
+        while (it.next(u)) {
+          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          for (int j = u.k0; j < u.k1; ++j, ++n) {
+            const uint32_t st = n % kSlots;
+            mbar_wait_backoff(BAR(kv_empty) + 8 * st, ((n / kSlots) & 1) ^ 1);
+            TRACE(TR_TMA, n);
+            const int row = __ldg(bt + j) * kPage;
+            const uint32_t dst = sbase + kOffKv + st * kStage;
+            const uint32_t full = BAR(kv_full) + 8 * st;
+            mbar_arrive_expect_tx(full, kKvTx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, full, c * 128, row, pol);
+            tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, full, 0, row, pol);
+            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 128, full, pol);
+            bulk_load(dst + kOffScaleHi, p.kv_scale + (int64_t)row + 32, 128, full, pol);
+          }
+        }
+      }
+    } else if (warp == kWarpQk) {
+      // ================================ QK issuer ================================
+      const uint64_t dQr = make_smem_desc(sbase + kOffQr, 16, 1024, LAYOUT_SW128);
+      uint32_t n = 0, unit = 0;
+      while (it.next(u)) {
+        mbar_wait(BAR(q_full), unit & 1, 2, unit);
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t st = n % kSlots, ss = n % kSSlots;
+          mbar_wait(BAR(kv_full) + 8 * st, (n / kSlots) & 1, 3, n);
+          mbar_wait(BAR(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
+          tc_fence_after();
+          if (lane == 0) TRACE(TR_QK, n);
+          const uint32_t kv = sbase + kOffKv + st * kStage;
+          qk_issue(tmem_S + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                   make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
+        }
+        mma_commit_ws(BAR(q_free));   // Q (TMEM + SMEM) reusable once this unit's QK MMAs completed
+        ++unit;
+      }
+    } else {
+      // =============================== PV_L / PV_R ===============================
+      const uint32_t half = warp - kWarpPv;
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t st = n % kSlots, ps = n % kPSlots;
+          const uint32_t h = 2 * n + half, ts = h % kTSlots;
+          mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);                  // P'(n) in SMEM
+          if (h >= kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / kTSlots - 1) & 1, 6, n);   // slot read
+          tc_fence_after();
+          if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+          const uint32_t pA = sbase + kOffP + ps * 4096;
+          const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
+          pv_issue(t_slot_addr(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                   make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
+                   BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
+        }
+      }
+    }
+  } else if (warp >= kWarpSoftmax) {
+    if constexpr (kRegsSoftmax > 128) regs_inc<kRegsSoftmax>();   // launch: 128 per thread
+    else regs_dec<kRegsSoftmax>();
+    // ======= softmax / scale fusion / P quantization: thread = (row, 32-token half) =======
     const int k = warp & 3;                  // TMEM subpartition of this warp
     const int t = lane & 15, hh = lane >> 4; // row-in-quarter, 32-token half
     const int r = 16 * k + t;                // query-head row inside the tile
@@ -424,14 +416,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_off = (uint32_t)(32 * k) << 16;
     const uint32_t stat0 = BAR(stat) + 4 * r;
-    const uint32_t set_bar = 1 + set;        // named barrier of the set (128 threads)
-    const uint64_t dQr = make_smem_desc(sbase + kOffQr, 16, 1024, LAYOUT_SW128);
     uint32_t n = 0, unit = 0;
     while (it.next(u)) {
-      const uint32_t n0 = n, nlast = n + (u.k1 - u.k0) - 1;
-      // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh.
-      // Both sets derive sigma_q (c_row); set 0 writes the codes (TMEM) and q_r' (SMEM).
-      if (set == 0 && unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // previous unit's QK done
+      // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh
+      if (unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // QK of the previous unit done
       float c_row;
       {
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
@@ -455,77 +443,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
         c_row = sq * p.scale_log2;
-        if (set == 0) {
-          // q_c codes -> TMEM (the QK A operand): this thread's 256 content bytes are TMEM
-          // columns kTmemQ + 64 hh + [0, 64) of its row, 4 codes per column (low byte first)
+        // q_c codes -> TMEM (the QK A operand): this thread's 256 content bytes are TMEM
+        // columns kTmemQ + 64 hh + [0, 64) of its row, 4 codes per column (low byte first)
 #pragma unroll
-          for (int half32 = 0; half32 < 2; ++half32) {
-            uint32_t qa[32];
+        for (int half32 = 0; half32 < 2; ++half32) {
+          uint32_t qa[32];
 #pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) {   // 16-byte chunk of codes (re-read: L1 hit)
-              const int gch = 8 * half32 + g8;
-              uint4 v2[2];
-              v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
-              v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
-              const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-                qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                                           div_by(f1.y, sq, rsq));
-              }
-            }
-            tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
-          }
-          tmem_wait_st();
-#pragma unroll
-          for (int gch = 0; gch < 4; ++gch) {
-            const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
-            const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-            uint32_t wd[4];
+          for (int g8 = 0; g8 < 8; ++g8) {   // 16-byte chunk of codes (re-read: L1 hit)
+            const int gch = 8 * half32 + g8;
+            uint4 v2[2];
+            v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
+            v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(a[e]);
-              __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                     __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-              wd[e] = *reinterpret_cast<uint32_t*>(&o2);
+              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+              qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                                         div_by(f1.y, sq, rsq));
             }
-            sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
           }
-          fence_proxy_async_smem();
-          tc_fence_before();
-          named_bar_sync(set_bar, 128);
-          if (k == 0) {   // Q complete: release set 1, then the unit's first two QKs
-            tc_fence_after();
-            if (lane == 0) mbar_arrive(BAR(q_full));
-            qk_block(n0, sbase, bar0, tmem, dQr);
-            if (n0 + 1 <= nlast) qk_block(n0 + 1, sbase, bar0, tmem, dQr);
-          }
-        } else if (k == 0) {
-          mbar_wait(BAR(q_full), unit & 1, 2, unit);   // the QKs this set issues read the new Q
+          tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
         }
+        tmem_wait_st();
+#pragma unroll
+        for (int gch = 0; gch < 4; ++gch) {
+          const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
+          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
+          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
+          uint32_t wd[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(a[e]);
+            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
+                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
+            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
+          }
+          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(q_full));
       }
 
       // visible keys of this row: query token t = head / heads of q_len sees the cache
       // up to its own position, L - (q_len - 1 - t) (causal MTP, reading R25)
       const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
+      // S(n) is loaded from TMEM one block ahead: the load of S(n+1) is issued before
+      // block n's P' / stats stores, fence and arrive, which hide its latency.
+      float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        if ((int)(n & 1) != set) continue;
         const uint32_t st = n % kSlots, ss = n % kSSlots, ps = n % kPSlots;
-        mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
-        tc_fence_after();
-        if (lane == 0 && k == 0) TRACE(TR_SM_IN, n);
-        float tt[32];
-        tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        if (j == u.k0) {
+          mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
+          tc_fence_after();
+          tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(s_empty) + 8 * ss);
-   // into the slot this set just read
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
         // sigma_K of my 32 tokens (from the TMA'd slot)
         const uint32_t sk = sbase + kOffKv + st * kStage + (hh ? kOffScaleHi : 5 * kBoxBytes);
-        const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the row's range
+        const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the sequence
         float4 skv[8];                                                 // sigma_K of my 32 tokens, kept
 #pragma unroll
         for (int e = 0; e < 8; ++e) skv[e] = lds_f4(sk + 16 * e);
@@ -551,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));          // block max of t (local m)
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S2, n);
         const float mc = mx == -INFINITY ? 0.f : mx * c_row;            // fully masked row block (MTP)
         float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
         float mb0 = 0.f, mb1 = 0.f;
@@ -576,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mb = fmaxf(mb0, mb1);
         mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
         // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
         // P' = 0 and is skipped by the recurrence (R11)
         const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
@@ -588,52 +572,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
           pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
         }
-        // P' / stats slot free once PV(n - 2) completed and the eight accumulator warps
-        // read its stats
-        if (lane == 0 && k == 0) TRACE(TR_S3, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
+        if (j + 1 < u.k1) {   // prefetch S(n+1)
+          const uint32_t ss1 = (n + 1) % kSSlots;
+          mbar_wait(BAR(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
+          tc_fence_after();
+          tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
+        // P' / stats slot free once PV_L and PV_R of block n - kPSlots completed and the
+        // eight accumulator warps read its stats
         mbar_wait(BAR(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
-        if (lane == 0 && k == 0) TRACE(TR_S4, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
+        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
         if (hh == 0) {
           const uint32_t sa = stat0 + ps * (3 * 64 * 4);
           sts_f32(sa, st_m);
           sts_f32(sa + 256, st_sig);
           sts_f32(sa + 512, lsum);
         }
-        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
         const uint32_t pdst = sbase + kOffP + ps * 4096 + r * 16;
         sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
         sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_C2, n);
         fence_proxy_async_smem();
-        named_bar_sync(set_bar, 128);                                  // P'(n) and stats complete
-        if (lane == 0 && k == 0) TRACE(TR_S5, n);
-        if (k == 0 && lane == 0) mbar_arrive(BAR(p_full) + 8 * ps);    // accumulator warps: stats
-        if (k == 0 && n + 2 <= nlast) {   // QK(n+2) into the S slot this set read (issue may block on a
-          qk_block(n + 2, sbase, bar0, tmem, dQr);   // full tensor queue: only the set's next block waits)
-          if (lane == 0) TRACE(TR_QK, n + 2);
-        }
-        if (k == 1) {                                                  // PV(n): both halves, one commit group
-          const uint32_t hl = 2 * n, hr = 2 * n + 1, tl = hl % kTSlots, tr = hr % kTSlots;
-          if (hl >= kTSlots) mbar_wait(BAR(t_free) + 8 * tl, (hl / kTSlots - 1) & 1, 6, n);
-          if (hr >= kTSlots) mbar_wait(BAR(t_free) + 8 * tr, (hr / kTSlots - 1) & 1, 6, n);
-          tc_fence_after();
-          if (lane == 0) TRACE(TR_PVL, n);
-          const uint32_t vb = sbase + kOffKv + st * kStage;
-          pv_issue2(t_slot_addr(tmem, tl), t_slot_addr(tmem, tr),
-                    make_smem_desc(sbase + kOffP + ps * 4096, 1024, 128, LAYOUT_NONE),
-                    make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128),
-                    make_smem_desc(vb + 2 * kBoxBytes, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * tl,
-                    BAR(t_full) + 8 * tr, BAR(p_empty) + 8 * ps);
-        }
-        if (lane == 0 && k == 0) TRACE(TR_SM_OUT, n);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(p_full) + 8 * ps);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
-      if (k == 0) mma_commit_ws(BAR(q_free));   // this warp's QKs of the unit done -> Q reusable
       ++unit;
     }
   } else {
     if constexpr (kRegsAcc > 128) regs_inc<kRegsAcc>();
     else regs_dec<kRegsAcc>();
     // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
-    const uint32_t w = (warp - kWarpAcc) >> 2;   // 0: O cols 0-255 (L halves), 1: cols 256-511 (R halves)
+    const uint32_t w = warp >> 2;            // 0: O cols 0-255 (L halves), 1: cols 256-511 (R halves)
     const int k = warp & 3;
     const int t = lane & 15, hh = lane >> 4;
     const int r = 16 * k + t;
@@ -641,23 +613,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_off = (uint32_t)(32 * k) << 16;
     const uint32_t stat0 = BAR(stat) + 4 * r;
-    // warp 4 (R half, subpartition 0) lane 0 is also the TMA producer: block n + kSlots is
-    // loaded into slot n % kSlots as soon as PV(n) completed (its t_full, which covers both
-    // halves: one commit group), the first kSlots blocks at start.
-    const bool producer = warp == kWarpAcc + 4 && lane == 0;
-    ProdIter pit{UnitIter{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0},
-                 Unit{}, 0, false};
-    uint32_t n_load = 0;
-    const uint64_t pol = producer ? l2_policy_evict_first() : 0;
-    if (producer) {
-      tma_prefetch_desc(&tm_kv);
-      tma_prefetch_desc(&tm_rope);
-      int pb, pj;
-      while (n_load < (uint32_t)kSlots && pit.next(pb, pj)) {
-        load_block(n_load % kSlots, pb, pj, p, sbase, bar0, &tm_kv, &tm_rope, pol);
-        ++n_load;
-      }
-    }
     uint32_t n = 0;
     while (it.next(u)) {
       const uint32_t n0 = n;
@@ -695,14 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t h = 2 * n + w, ts = h % kTSlots;
         mbar_wait(BAR(t_full) + 8 * ts, (h / kTSlots) & 1, 10, n);      // T half = P'(n) V complete
         tc_fence_after();
-        if (producer) {   // PV(n) done: slot n % kSlots is free -> block n + kSlots
-          int pb, pj;
-          if (pit.next(pb, pj)) {
-            load_block(n_load % kSlots, pb, pj, p, sbase, bar0, &tm_kv, &tm_rope, pol);
-            ++n_load;
-          }
-        }
-        if (threadIdx.x == 32 * kWarpAcc + 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
         const uint32_t taddr = t_slot_addr(tmem, ts) + lane_off;
         const float2 g2 = make_float2(gamma, gamma);
         // software-pipelined T reads (8 chunks of 16 columns)
@@ -728,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (threadIdx.x == 32 * kWarpAcc + 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
       }
       // ---------------- epilogue (a9): o = sig_O 2^{m_O - m_ref} O / l ; L = (m_ref + log2 l) ln 2
       // a row that saw no key in this split (MTP: the split holds only keys after its
@@ -752,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kWarpSm) {
+  if (warp == kWarpQk) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
