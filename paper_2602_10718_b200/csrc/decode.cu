@@ -74,6 +74,8 @@ constexpr uint32_t kIdescPv = make_idesc(0, 0, 0, 1, 64, 256);      // P' K-majo
 
 struct DecodeParams {
   const __nv_bfloat16* q;
+  const uint8_t* kv_fp8;         // pools (L2 prefetch addresses; the loads go through the tensor maps)
+  const __nv_bfloat16* kv_rope;
   const float* kv_scale;
   const int32_t* block_table;
   const int32_t* seq_lens;
@@ -713,6 +715,590 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 }
 
+// ===================================================================== CTA-pair kernel
+// 64 < rows <= 128 (DeepSeek-R1's 128 heads): the two head tiles of a key range run as
+// a CTA pair (cluster of 2) and share the QK tensor work through cta_group::2 MMAs.
+// Measured data path (scripts/pair_probe.cu): for cta_group::2, M = 128 (64 rows per CTA),
+// CTA c holds D[row r, col n] at lane r for n < N/2 (B columns supplied by CTA 0) and at
+// lane 64 + r, column n - N/2 for n >= N/2 (B columns supplied by CTA 1).  So one pair QK
+// of N = 128 over TWO key blocks -- block A from CTA 0's SMEM, block B from CTA 1's -- leaves
+// every CTA with S(A) for its 64 rows on lanes 0-63 and S(B) on lanes 64-127: the softmax of
+// block A runs on SMSPs 0-1 and that of block B on SMSPs 2-3, one thread per (row, block)
+// with all 64 tokens in-thread (no shuffles).  The QK costs 32 instead of 64 cycles per
+// 32-byte K chunk per block (tcgen05 floor max(M,128) N / (256 cta_group)).
+// PV stays per CTA (cta_group::1, M = 64, P' x V of its own rows; mixing both groups in one
+// kernel is validated by the same probe) into 6 quarter tiles (64 x 128) of TMEM.
+// Pair SMEM slot = two 41 KB sub-slots; CTA 0 keeps block A in sub-slot 0, CTA 1 keeps
+// block B there, so the leader's QK operand address is the same in both CTAs.
+// Cross-CTA traffic per block pair: the peer's sub-slot-0 TMA completes on the leader's
+// barrier (cta_group::2 TMA), the peer's four softmax warps arrive (relaxed) on the
+// leader's s_empty, and the QK commit multicasts s_full to both CTAs.  Once per unit the
+// peer's Q-quant prologue arrives (release) on the leader's q_full.
+constexpr int kPairSlots = 2;                        // KV ring depth (block pairs)
+constexpr int kPrefetchPairs = 2;                    // L2 prefetch distance (block pairs)
+constexpr int kQSlots = 6;                           // TMEM ring of 64 x 128 PV quarter tiles
+constexpr uint32_t kPairStage = 2 * kStage;          // two blocks
+constexpr uint32_t kPOffQc = 0;                      // q_c codes: 4 SW128 boxes [64 rows x 128 B]
+constexpr uint32_t kPOffQr = 32768;                  // q_r / sigma_q (BF16, SW128)
+constexpr uint32_t kPOffP = 40960;                   // P' 2 slots x 4096
+constexpr uint32_t kPOffKv = 49152;
+constexpr uint32_t kPOffBar = kPOffKv + kPairSlots * kPairStage;
+constexpr uint32_t kPSmemBytes = kPOffBar + 4096 + 1024;
+static_assert(kPSmemBytes <= 232448, "shared memory budget (pair kernel)");
+constexpr uint32_t kTxSub0 = 4 * kBoxBytes + kBoxBytes;   // content + RoPE of one block (QK operand)
+constexpr uint32_t kIdescQk8P = make_idesc(0, 0, 0, 0, 128, 128);
+constexpr uint32_t kIdescQk16P = make_idesc(1, 1, 0, 0, 128, 128);
+constexpr uint32_t kIdescPvQ = make_idesc(0, 0, 0, 1, 64, 128);
+// registers (setmaxnreg, per SMSP 2 acc + 1 issue + 1 softmax warp): the pair softmax holds a
+// whole 64-token row per thread, the accumulators read T in 8-column chunks
+constexpr uint32_t kPRegsAcc = 168, kPRegsSoftmax = 136;
+static_assert(2 * 32 * kPRegsAcc + 32 * kRegsIssue + 32 * kPRegsSoftmax <= 4 * 32 * 128, "pair register budget");
+
+struct PairBars {
+  uint64_t kvq_full[kPairSlots];   // sub-slot 0 of both CTAs landed (leader)
+  uint64_t kvl_full[kPairSlots];   // sub-slot 1 content of this CTA landed
+  uint64_t sc_full[kPairSlots];    // sigma_K of both blocks landed (loaded first: the softmax needs only these)
+  uint64_t kv_empty[kPairSlots];   // PV_L + PV_R of the pair's last block completed
+  uint64_t s_full[kSSlots], s_empty[kSSlots];
+  uint64_t p_full[kPSlots], p_empty[kPSlots];
+  uint64_t t_full[kQSlots], t_free[kQSlots];
+  uint64_t q_full, q_free;
+  uint32_t tmem_base;
+  float crow[64];
+  float stat[kPSlots][3][64];
+};
+static_assert(sizeof(PairBars) <= 4096, "barrier region (pair kernel)");
+#define PBAR(field) (bar0 + (uint32_t)offsetof(PairBars, field))
+
+// One pair QK (leader only): S[ss] (+)= q_c x K_c^T (16 x K = 32, A and B from SMEM)
+// + q_r' x K_r'^T (4 x K = 16), cta_group::2, M = 128, N = 128; commit multicast to both CTAs.
+#define SNAPMLA_QK8P(o, acc)                                                                   \
+  "add.s64 a, %1, " #o ";\n\tadd.s64 b, %2, " #o ";\n\t"                                       \
+  "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], a, b, %3, " acc ";\n\t"
+#define SNAPMLA_QK16P(o)                                                                       \
+  "add.s64 a, %4, " #o ";\n\tadd.s64 b, %5, " #o ";\n\t"                                       \
+  "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %6, pt;\n\t"
+__device__ __forceinline__ void qk_issue_pair(uint32_t dS, uint64_t dQc, uint64_t dK, uint64_t dQr, uint64_t dKr,
+                                              uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      SNAPMLA_QK8P(0, "pf") SNAPMLA_QK8P(2, "pt") SNAPMLA_QK8P(4, "pt") SNAPMLA_QK8P(6, "pt")
+      SNAPMLA_QK8P(512, "pt") SNAPMLA_QK8P(514, "pt") SNAPMLA_QK8P(516, "pt") SNAPMLA_QK8P(518, "pt")
+      SNAPMLA_QK8P(1024, "pt") SNAPMLA_QK8P(1026, "pt") SNAPMLA_QK8P(1028, "pt") SNAPMLA_QK8P(1030, "pt")
+      SNAPMLA_QK8P(1536, "pt") SNAPMLA_QK8P(1538, "pt") SNAPMLA_QK8P(1540, "pt") SNAPMLA_QK8P(1542, "pt")
+      SNAPMLA_QK16P(0) SNAPMLA_QK16P(2) SNAPMLA_QK16P(4) SNAPMLA_QK16P(6)
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %8;\n\t}"
+      ::"r"(dS), "l"(dQc), "l"(dK), "r"(kIdescQk8P), "l"(dQr), "l"(dKr), "r"(kIdescQk16P), "r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// One PV quarter (cta_group::1): T = P' (64 x 64 tokens, K-major) x V (64 tokens x 128 dims,
+// MN-major), 2 x K = 32; commit to t_full.
+__device__ __forceinline__ void pv_issue_quarter(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPvQ), "r"(bar_t)
+      : "memory");
+}
+
+// TMEM (pair kernel): S pair slots at cols 64 ss (all 128 lanes); PV quarter slot s at
+// lane group 16 (s & 1) (M = 64 layout), cols 128 + 128 (s >> 1).
+__device__ __forceinline__ uint32_t q_slot_addr(uint32_t tmem, uint32_t s) {
+  return tmem + ((s & 1u) ? (16u << 16) : 0u) + 128u + 128u * (s >> 1);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mla_decode_pair_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
+                           const DecodeParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = sbase + kPOffBar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();   // == head tile
+  const bool leader = cta == 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPairSlots; ++i) {
+      mbar_init(PBAR(kvq_full) + 8 * i, 1);
+      mbar_init(PBAR(kvl_full) + 8 * i, 1);
+      mbar_init(PBAR(sc_full) + 8 * i, 1);
+      mbar_init(PBAR(kv_empty) + 8 * i, 2);
+    }
+    for (int i = 0; i < kSSlots; ++i) {
+      mbar_init(PBAR(s_full) + 8 * i, 1);
+      mbar_init(PBAR(s_empty) + 8 * i, 8);      // 4 local + 4 peer softmax warps (leader's copy is used)
+    }
+    for (int i = 0; i < kPSlots; ++i) {
+      mbar_init(PBAR(p_full) + 8 * i, 2);       // the two softmax warps of the block's parity
+      mbar_init(PBAR(p_empty) + 8 * i, 2 + 8);  // PV_L + PV_R commits, 8 accumulator warps
+    }
+    for (int i = 0; i < kQSlots; ++i) {
+      mbar_init(PBAR(t_full) + 8 * i, 1);
+      mbar_init(PBAR(t_free) + 8 * i, 4);
+    }
+    mbar_init(PBAR(q_full), 8);                 // 4 local + 4 peer prologue warps
+    mbar_init(PBAR(q_free), 1);
+    fence_barrier_init();
+  }
+  if (warp == kWarpTma && lane == 0) {
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_rope);
+  }
+  if (warp == kWarpQk) tmem_alloc_pair(PBAR(tmem_base), 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // peer barriers initialised before any remote arrive / TMA completion
+  tc_fence_after();
+  const uint32_t tmem = lds_u32(PBAR(tmem_base));
+
+  pdl_wait();
+  const int ht = (int)cta;
+  const int g = blockIdx.x / 2;
+  const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
+  const int lo = g * per;
+  const bool has_work = g < groups && lo < total;
+  const int hi = min(total, lo + per);
+#ifdef SNAPMLA_TRACE
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x] = gt;
+  }
+#endif
+  UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
+  Unit u;
+  // sub-slot of block A (k0 + 2i) / B (k0 + 2i + 1) in this CTA
+  const uint32_t subA = leader ? 0u : 1u;
+
+  if (warp >= kWarpTma && warp < kWarpSoftmax) {
+    regs_dec<kRegsIssue>();
+    if (warp == kWarpTma) {
+      // ============================ TMA producer (per block pair) ============================
+      if (lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        const uint32_t kvq_leader0 = mapa_shared(PBAR(kvq_full), 0);
+        uint32_t np = 0;
+        while (it.next(u)) {
+          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
+            const bool hasB = jA + 1 < u.k1;
+            const uint32_t st = np % kPairSlots;
+            mbar_wait_backoff(PBAR(kv_empty) + 8 * st, ((np / kPairSlots) & 1) ^ 1);
+            TRACE(TR_TMA, np);
+            const uint32_t slot = sbase + kPOffKv + st * kPairStage;
+            const int rowA = __ldg(bt + jA) * kPage;
+            const int rowB = hasB ? __ldg(bt + jA + 1) * kPage : 0;
+            // L2 prefetch kPrefetchPairs pairs ahead (this CTA: its sub-slot-0 block), so the
+            // TMA of a recycled slot hits L2 instead of waiting a full DRAM round trip
+            {
+              const int jp = jA + 2 * kPrefetchPairs + (leader ? 0 : 1);
+              if (jA == u.k0) {   // unit start: the first pairs too
+                for (int jj = jA + 2 + (leader ? 0 : 1); jj < min(jp, u.k1); jj += 2) {
+                  const int64_t rp = (int64_t)__ldg(bt + jj) * kPage;
+                  bulk_prefetch_l2(p.kv_fp8 + rp * kDc, kPage * kDc);
+                  bulk_prefetch_l2(p.kv_rope + rp * kDr, kPage * kDr * 2);
+                }
+              }
+              if (jp < u.k1) {
+                const int64_t rp = (int64_t)__ldg(bt + jp) * kPage;
+                bulk_prefetch_l2(p.kv_fp8 + rp * kDc, kPage * kDc);
+                bulk_prefetch_l2(p.kv_rope + rp * kDr, kPage * kDr * 2);
+              }
+            }
+            // sub-slot 0: the QK operand (leader: block A, peer: block B), counted on the leader's barrier
+            if (leader) mbar_arrive_expect_tx(PBAR(kvq_full) + 8 * st, kTxSub0 * (hasB ? 2u : 1u));
+            // scales first (local): the softmax waits only for these
+            const uint32_t sc_bar = PBAR(sc_full) + 8 * st;
+            const uint32_t sA = slot + subA * kStage, sB = slot + (1u - subA) * kStage;
+            mbar_arrive_expect_tx(sc_bar, 256u * (hasB ? 2u : 1u));
+            bulk_load(sA + 5 * kBoxBytes, p.kv_scale + (int64_t)rowA, 128, sc_bar, pol);
+            bulk_load(sA + kOffScaleHi, p.kv_scale + (int64_t)rowA + 32, 128, sc_bar, pol);
+            if (hasB) {
+              bulk_load(sB + 5 * kBoxBytes, p.kv_scale + (int64_t)rowB, 128, sc_bar, pol);
+              bulk_load(sB + kOffScaleHi, p.kv_scale + (int64_t)rowB + 32, 128, sc_bar, pol);
+            }
+            const int row0 = leader ? rowA : rowB;
+            const uint32_t q_bar = kvq_leader0 + 8 * st;
+            if (leader || hasB) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) tma_load_2d_cg2(slot + c * kBoxBytes, &tm_kv, q_bar, c * 128, row0, pol);
+              tma_load_2d_cg2(slot + 4 * kBoxBytes, &tm_rope, q_bar, 0, row0, pol);
+            }
+            // local: sub-slot 1 content (the other block's V)
+            const bool has1 = leader ? hasB : true;
+            const int row1 = leader ? rowB : rowA;
+            const uint32_t l_bar = PBAR(kvl_full) + 8 * st;
+            mbar_arrive_expect_tx(l_bar, has1 ? 4 * kBoxBytes : 0u);   // armed every pair (phase = pair count)
+            if (has1) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                tma_load_2d(slot + kStage + c * kBoxBytes, &tm_kv, l_bar, c * 128, row1, pol);
+            }
+          }
+        }
+      }
+    } else if (warp == kWarpQk) {
+      // ================================ pair QK issuer (leader) ================================
+      if (leader) {
+        const uint64_t dQc = make_smem_desc(sbase + kPOffQc, 16, 1024, LAYOUT_SW128);
+        const uint64_t dQr = make_smem_desc(sbase + kPOffQr, 16, 1024, LAYOUT_SW128);
+        uint32_t np = 0, unit = 0;
+        while (it.next(u)) {
+          mbar_wait(PBAR(q_full), unit & 1, 2, unit);
+          for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
+            const uint32_t st = np % kPairSlots, ss = np % kSSlots;
+            mbar_wait(PBAR(kvq_full) + 8 * st, (np / kPairSlots) & 1, 3, np);
+            if (lane == 0) TRACE(TR_S2, np);
+            mbar_wait(PBAR(s_empty) + 8 * ss, ((np / kSSlots) & 1) ^ 1, 4, np);
+            tc_fence_after();
+            if (lane == 0) TRACE(TR_QK, np);
+            const uint32_t kv = sbase + kPOffKv + st * kPairStage;
+            qk_issue_pair(tmem + 64 * ss, dQc, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                          make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), PBAR(s_full) + 8 * ss);
+          }
+          mma_commit_pair_ws(PBAR(q_free));   // both CTAs' Q reusable once this unit's QK completed
+          ++unit;
+        }
+      }
+    } else {
+      // ============================ PV_L / PV_R (per CTA, quarters) ============================
+      const uint32_t half = warp - kWarpPv;
+      uint32_t n = 0, np = 0;
+      while (it.next(u)) {
+        for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
+          const int nb = jA + 1 < u.k1 ? 2 : 1;
+          const uint32_t st = np % kPairSlots;
+          for (int b = 0; b < nb; ++b, ++n) {
+            const uint32_t ps = n % kPSlots;
+            mbar_wait(PBAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
+            if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+            const uint32_t pA = sbase + kPOffP + ps * 4096;
+            const uint32_t sub = b == 0 ? subA : 1u - subA;
+            if (sub == 1) mbar_wait(PBAR(kvl_full) + 8 * st, (np / kPairSlots) & 1, 13, n);   // V of sub-slot 1
+            const uint32_t vb = sbase + kPOffKv + st * kPairStage + sub * kStage + (2 * half) * kBoxBytes;
+#pragma unroll
+            for (int qi = 0; qi < 2; ++qi) {
+              const uint32_t q = 4 * n + 2 * half + qi, qs = q % kQSlots;
+              if (q >= kQSlots) mbar_wait(PBAR(t_free) + 8 * qs, (q / kQSlots - 1) & 1, 6, n);
+              tc_fence_after();
+              pv_issue_quarter(q_slot_addr(tmem, qs), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                               make_smem_desc(vb + qi * kBoxBytes, kBoxBytes, 1024, LAYOUT_SW128),
+                               PBAR(t_full) + 8 * qs);
+            }
+            mma_commit_ws(PBAR(p_empty) + 8 * ps);
+            if (b == nb - 1) mma_commit_ws(PBAR(kv_empty) + 8 * st);
+          }
+        }
+      }
+    }
+  } else if (warp >= kWarpSoftmax) {
+    regs_inc<kPRegsSoftmax>();
+    const int k = warp & 3;
+    // ---- prologue mapping (as the single-CTA kernel): row r = 16k + t, content half hh
+    const int t = lane & 15, hh = lane >> 4;
+    const int r = 16 * k + t;
+    const int head = ht * kHeadTile + r;
+    const bool row_ok = head < p.num_heads;
+    // ---- softmax mapping: block parity par (A: SMSPs 0-1, B: 2-3), row rho, all 64 tokens
+    const int par = k >> 1;
+    const int rho = 32 * (k & 1) + lane;
+    const int head_s = ht * kHeadTile + rho;
+    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
+    const uint32_t s_empty_leader = mapa_shared(PBAR(s_empty), 0);
+    const uint32_t q_full_leader = mapa_shared(PBAR(q_full), 0);
+    uint32_t n = 0, np = 0, unit = 0;
+    while (it.next(u)) {
+      // ---------------- Fused-Q-Quant prologue (a2): codes + q_r' into this CTA's SMEM
+      if (unit > 0) {
+        mbar_wait(PBAR(q_free), (unit - 1) & 1, 11, unit);
+        named_bar_sync(1, 128);   // every softmax warp read the previous unit's crow
+      }
+      {
+        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
+        float amax = 0.f;
+#pragma unroll
+        for (int bh = 0; bh < 4; ++bh) {
+          uint4 qv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * hh + 8 * bh + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(hv[e]);
+              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+            }
+          }
+        }
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
+        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
+        const float rsq = __frcp_rn(sq);
+        if (hh == 0) sts_f32(PBAR(crow) + 4 * r, sq * p.scale_log2);
+        // this thread's 256 content bytes = SW128 boxes 2 hh, 2 hh + 1 of row r
+#pragma unroll
+        for (int half32 = 0; half32 < 2; ++half32) {
+          const uint32_t box = sbase + kPOffQc + (2 * hh + half32) * kBoxBytes + r * 128;
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            const int gch = 8 * half32 + g8;
+            uint4 v2[2];
+            v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
+            v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+              w4[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                                div_by(f1.y, sq, rsq));
+            }
+            sts_u4(box + ((g8 ^ (r & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
+          }
+        }
+#pragma unroll
+        for (int gch = 0; gch < 4; ++gch) {
+          const int c = 4 * hh + gch;
+          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
+          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
+          uint32_t wd[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(a[e]);
+            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
+                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
+            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
+          }
+          sts_u4(sbase + kPOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(PBAR(q_full));
+          else mbar_arrive_cluster(q_full_leader);   // release: Q codes published to the leader's MMA
+        }
+      }
+      named_bar_sync(1, 128);   // crow of every row written
+      const float c_row = lds_f32(PBAR(crow) + 4 * rho);
+      const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head_s / p.heads);
+
+      float tt[64];
+      for (int jA = u.k0; jA < u.k1; n += (jA + 1 < u.k1 ? 2 : 1), jA += 2, ++np) {
+        const int nb = jA + 1 < u.k1 ? 2 : 1;
+        const bool mine = par < nb;
+        const uint32_t ss = np % kSSlots, st = np % kPairSlots;
+        mbar_wait(PBAR(s_full) + 8 * ss, (np / kSSlots) & 1, 7, np);
+        tc_fence_after();
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, np);
+        if (threadIdx.x == 32 * kWarpSoftmax + 64) TRACE(TR_S3, np);
+        if (mine) {
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss + 32, *reinterpret_cast<uint32_t(*)[32]>(tt + 32));
+          tmem_wait_ld();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(PBAR(s_empty) + 8 * ss);
+          else mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
+        }
+        if (!mine) continue;
+        const uint32_t nm = n + par, ps = nm % kPSlots;
+        const int j = jA + par;
+        mbar_wait(PBAR(sc_full) + 8 * st, (np / kPairSlots) & 1, 12, np);   // sigma_K landed
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, np);
+        const uint32_t sub = par == 0 ? subA : 1u - subA;
+        const uint32_t skA = sbase + kPOffKv + st * kPairStage + sub * kStage;
+        const int nvalid = L - j * kBc;
+        // Alg.1 step 3 (descale) with sigma_K read from SMEM (broadcast)
+#pragma unroll
+        for (int e = 0; e < 64; e += 4)
+          lds_mul4(skA + (e < 32 ? 5 * kBoxBytes + 4 * e : kOffScaleHi + 4 * (e - 32)), tt[e], tt[e + 1], tt[e + 2],
+                   tt[e + 3]);
+        if (nvalid < 64) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
+        }
+        float m4[4] = {tt[0], tt[1], tt[2], tt[3]};
+#pragma unroll
+        for (int e = 4; e < 64; e += 4) {
+          m4[0] = fmaxf(m4[0], tt[e]);
+          m4[1] = fmaxf(m4[1], tt[e + 1]);
+          m4[2] = fmaxf(m4[2], tt[e + 2]);
+          m4[3] = fmaxf(m4[3], tt[e + 3]);
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        const float mc = mx == -INFINITY ? 0.f : mx * c_row;
+        float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+        float mb0 = 0.f, mb1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));
+          const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
+          ls0 = __fadd2_rn(ls0, p0);
+          ls1 = __fadd2_rn(ls1, p1);
+          float2 w0 = p0, w1 = p1;
+          lds_mul4(skA + (e < 32 ? 5 * kBoxBytes + 4 * e : kOffScaleHi + 4 * (e - 32)), w0.x, w0.y, w1.x, w1.y);
+          tt[e] = w0.x;
+          tt[e + 1] = w0.y;
+          tt[e + 2] = w1.x;
+          tt[e + 3] = w1.y;
+          mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
+          mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
+        }
+        const float lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
+        const float mb = fmaxf(mb0, mb1);
+        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
+        const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
+        const float2 inv2 = make_float2(inv, inv);
+        uint32_t pw[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
+          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
+          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+        }
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, np);
+        mbar_wait(PBAR(p_empty) + 8 * ps, ((nm / kPSlots) & 1) ^ 1, 8, nm);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, np);
+        const uint32_t sa = PBAR(stat) + ps * (3 * 64 * 4) + 4 * rho;
+        sts_f32(sa, st_m);
+        sts_f32(sa + 256, st_sig);
+        sts_f32(sa + 512, lsum);
+        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
+        const uint32_t pdst = sbase + kPOffP + ps * 4096 + rho * 16;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sts_u4(pdst + c * 1024, pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(PBAR(p_full) + 8 * ps);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, np);
+        if (threadIdx.x == 32 * kWarpSoftmax + 64) TRACE(TR_C2, np);
+      }
+      ++unit;
+    }
+  } else {
+    regs_inc<kPRegsAcc>();
+    // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
+    // WG w owns dims [256 w, 256 w + 256) = quarters 2w, 2w+1; thread (row r, hh) holds
+    // dims 256 w + 128 qi + 64 hh + [0, 64) in o[64 qi + ...]
+    const uint32_t w = warp >> 2;
+    const int k = warp & 3;
+    const int t = lane & 15, hh = lane >> 4;
+    const int r = 16 * k + t;
+    const int head = ht * kHeadTile + r;
+    const bool row_ok = head < p.num_heads;
+    const uint32_t lane_off = (uint32_t)(32 * k) << 16;
+    const uint32_t stat0 = PBAR(stat) + 4 * r;
+    uint32_t n = 0;
+    while (it.next(u)) {
+      const uint32_t n0 = n;
+      float o[128];
+#pragma unroll
+      for (int e = 0; e < 128; ++e) o[e] = 0.f;
+      float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        const uint32_t ps = n % kPSlots;
+        mbar_wait(PBAR(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
+        const uint32_t sa = stat0 + ps * (3 * 64 * 4);
+        const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(PBAR(p_empty) + 8 * ps);
+        const float m_new = fmaxf(m_ref, mb);
+        const bool first = n == n0;
+        const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
+        float gamma = 0.f;
+        if (first) {
+          m_O = mb;
+          sig_O = sb;
+          l_run = lb;
+          m_ref = mb;
+        } else if (!skip) {
+          gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);
+          l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
+          m_ref = m_new;
+          m_O = mb;
+          sig_O = sb;
+        }
+        const float2 g2 = make_float2(gamma, gamma);
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+          const uint32_t q = 4 * n + 2 * w + qi, qs = q % kQSlots;
+          mbar_wait(PBAR(t_full) + 8 * qs, (q / kQSlots) & 1, 10, n);
+          tc_fence_after();
+          const uint32_t taddr = q_slot_addr(tmem, qs) + lane_off;
+          uint32_t tv[2][8];
+          tmem_ld_16x32bx2_x8<64>(taddr, tv[0]);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            tmem_wait_ld();
+            if (c < 7) tmem_ld_16x32bx2_x8<64>(taddr + 8 * (c + 1), tv[(c + 1) & 1]);
+            else {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(PBAR(t_free) + 8 * qs);
+            }
+            const uint32_t* cur = tv[c & 1];
+            if (!skip) {
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const int oi = 64 * qi + 8 * c + e;
+                const float2 a = __ffma2_rn(make_float2(o[oi], o[oi + 1]), g2,
+                                            make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
+                o[oi] = a.x;
+                o[oi + 1] = a.y;
+              }
+            }
+          }
+        }
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
+      }
+      const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;
+      (void)0;
+      const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
+      if (row_ok) {
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+          float* dst = p.o_part + prow * kDc + 256 * w + 128 * qi + 64 * hh;
+#pragma unroll
+          for (int e = 0; e < 64; e += 4)
+            *reinterpret_cast<float4*>(dst + e) = make_float4(o[64 * qi + e] * f, o[64 * qi + e + 1] * f,
+                                                              o[64 * qi + e + 2] * f, o[64 * qi + e + 3] * f);
+        }
+        if (w == 0 && hh == 0)
+          p.lse_part[prow] = l_run > 0.f ? (m_ref + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // the leader's last pair MMAs (into the peer's TMEM) are complete on both sides
+  if (warp == kWarpQk) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+#ifdef SNAPMLA_TRACE
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x + 1] = gt;
+  }
+#endif
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -745,6 +1331,8 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 }
 
 static unsigned long long* g_trace = nullptr;
+static bool g_pair = false;   // experimental CTA-pair kernel for 64 < rows <= 128
+static int g_pair_groups = 0, g_pair_max_clusters = -1;   // debug: force the single-CTA kernel for 64 < rows <= 128
 
 int device_num_sms() {
   int dev = 0, n = 0;
@@ -759,6 +1347,15 @@ using namespace snapmla;
 
 // Debug only (include/snapmla_debug.h): subsequent decodes record a CTA-0 event timeline.
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
+// Experimental: 1 = run 64 < rows <= 128 on the CTA-pair kernel instead of the default single-CTA
+// kernel (two CTAs per key range, each with its own M = 64 QK).
+extern "C" void mla_debug_set_pair(int v) { g_pair = v != 0; }
+// Debug only: cap the number of CTA pairs of the pair kernel (0 = all that fit); returns the
+// occupancy limit cudaOccupancyMaxActiveClusters reported on the last pair launch (-1: none yet).
+extern "C" int mla_debug_set_pair_groups(int v) {
+  g_pair_groups = v;
+  return g_pair_max_clusters;
+}
 
 extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms) {
   if (batch < 0 || num_heads <= 0) return 0;
@@ -789,7 +1386,26 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   if (workspace_bytes < wl.total) return MLA_ERR_WORKSPACE;
   const int n_ht = (num_heads + kHeadTile - 1) / kHeadTile;
-  const int groups = sms / n_ht;
+  const bool pair = n_ht == 2 && g_pair;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
+  int groups = sms / n_ht;
+  if (pair) {
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      if (cudaFuncSetAttribute(mla_decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemBytes) !=
+          cudaSuccess)
+        return MLA_ERR_CUDA;
+      cudaLaunchConfig_t oc = {};
+      oc.gridDim = dim3(2 * groups);
+      oc.blockDim = dim3(kThreads);
+      oc.dynamicSmemBytes = kPSmemBytes;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, mla_decode_pair_kernel, &oc) != cudaSuccess) return MLA_ERR_CUDA;
+      max_clusters = nc;
+    }
+    g_pair_max_clusters = max_clusters;
+    if (max_clusters > 0 && max_clusters < groups) groups = max_clusters;
+    if (g_pair_groups > 0 && g_pair_groups < groups) groups = g_pair_groups;
+  }
 
   CUtensorMap tm_kv, tm_rope;
   const uint64_t rows = (uint64_t)num_pages * kPage;
@@ -806,11 +1422,13 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   plan_kernel<<<1, 1024, 0, st>>>(seq_lens, batch, num_heads, groups, hdr, cum, first);
   if (cudaGetLastError() != cudaSuccess) return MLA_ERR_CUDA;
 
-  if (cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+  if (!pair && cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
       cudaSuccess)
     return MLA_ERR_CUDA;
   DecodeParams prm;
   prm.q = (const __nv_bfloat16*)q;
+  prm.kv_fp8 = kv_fp8;
+  prm.kv_rope = (const __nv_bfloat16*)kv_rope;
   prm.kv_scale = kv_scale;
   prm.block_table = block_table;
   prm.seq_lens = seq_lens;
@@ -833,14 +1451,18 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * n_ht);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = pair ? kPSmemBytes : kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, mla_decode_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
+  if (pair) {
+    if (cudaLaunchKernelEx(&cfg, mla_decode_pair_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
+  } else if (cudaLaunchKernelEx(&cfg, mla_decode_kernel, tm_kv, tm_rope, prm) != cudaSuccess) {
+    return MLA_ERR_CUDA;
+  }
   return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
 }
 

@@ -187,6 +187,16 @@ DEVI float4 lds_f4(uint32_t saddr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
   return v;
 }
+// x[0..3] *= the four fp32 at saddr (load and use in one asm block: the compiler cannot
+// hoist the load and keep 4 extra registers live across an unrolled loop)
+DEVI void lds_mul4(uint32_t saddr, float& a, float& b, float& c, float& d) {
+  asm volatile(
+      "{\n\t.reg .f32 s0, s1, s2, s3;\n\t"
+      "ld.shared.v4.f32 {s0, s1, s2, s3}, [%4];\n\t"
+      "mul.rn.f32 %0, %0, s0;\n\tmul.rn.f32 %1, %1, s1;\n\tmul.rn.f32 %2, %2, s2;\n\tmul.rn.f32 %3, %3, s3;\n\t}"
+      : "+f"(a), "+f"(b), "+f"(c), "+f"(d)
+      : "r"(saddr));
+}
 DEVI uint32_t lds_u32(uint32_t saddr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
@@ -237,6 +247,16 @@ DEVI void tma_load_2d(uint32_t dst, const void* desc, uint32_t bar, int32_t x, i
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(x), "r"(y), "r"(bar), "l"(policy)
       : "memory");
 }
+// CTA-pair form: the load lands in this CTA's SMEM, its completion is counted on the
+// mbarrier at shared::cluster address `bar_cluster` (the pair leader's barrier)
+DEVI void tma_load_2d_cg2(uint32_t dst, const void* desc, uint32_t bar_cluster, int32_t x, int32_t y,
+                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(x), "r"(y), "r"(bar_cluster), "l"(policy)
+      : "memory");
+}
 DEVI void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
@@ -248,6 +268,11 @@ DEVI void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// bulk prefetch of [src, src + bytes) into L2 (no SMEM, no barrier)
+DEVI void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
 }
 DEVI uint64_t l2_policy_evict_first() {
   uint64_t p;
@@ -267,6 +292,26 @@ DEVI void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+// CTA pair (cta_group::2): one warp of EACH CTA of the pair executes these
+DEVI void tmem_alloc_pair(uint32_t dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+DEVI void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// completion of this thread's prior cta_group::2 MMAs -> arrive on the barrier at the same
+// offset in both CTAs of the pair
+DEVI void mma_commit_pair_ws(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          bar),
+      "h"((uint16_t)3)
+      : "memory");
 }
 DEVI void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
@@ -356,6 +401,13 @@ DEVI void tmem_ld_16x32bx2_x16(uint32_t taddr, uint32_t (&r)[16]) {
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16], %17;"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr), "n"(SPLIT));
+}
+template <int SPLIT>
+DEVI void tmem_ld_16x32bx2_x8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
       : "r"(taddr), "n"(SPLIT));
 }
 // 32 lanes x N columns: thread i reads lane base+i, columns [col, col+N)

@@ -52,6 +52,10 @@ def lib():
     L.mla_combine.argtypes = [_P, _I, _I, _I, _P, _P, _P]
     L.mla_combine_f32.restype = _I
     L.mla_combine_f32.argtypes = [_P, _I, _I, _I, _P, _P, _P]
+    if os.environ.get("SNAPMLA_PAIR") == "1":   # experimental CTA-pair kernel (include/snapmla_debug.h)
+        L.mla_debug_set_pair(1)
+    if os.environ.get("SNAPMLA_PAIR_GROUPS"):
+        L.mla_debug_set_pair_groups(int(os.environ["SNAPMLA_PAIR_GROUPS"]))
     _lib = L
     return L
 
