@@ -15,6 +15,7 @@ all-gathers the output over NCCL.
   python bench.py --mtp 2            # NEXT-1: q_len = 2 query tokens per request
   python bench.py --sweep            # BASELINE.json configs[4]: DeepSeek-R1 shape, context x batch grid
   python bench.py --fetch            # NEXT-3: Fused-Fetch-Dequant of the whole workload cache (GB/s)
+  python bench.py --bf16             # NEXT-2: unquantized BF16 baseline decode (1152 B / token) for the FP8/BF16 ratio
 """
 import argparse
 import json
@@ -58,6 +59,8 @@ def parse():
                     help="profiling runs: no clock-settle loop, no e2e leg, no cpu baseline")
     ap.add_argument("--mtp", type=int, default=1, help="query tokens per request per step (MTP, NEXT-1)")
     ap.add_argument("--fetch", action="store_true", help="time mla_kv_fetch_dequant over the workload cache")
+    ap.add_argument("--bf16", action="store_true",
+                    help="NEXT-2: the unquantized BF16 baseline (mla_decode_bf16, same skeleton) on the same workload")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE.json configs[4]: DeepSeek-R1 shape over contexts 4K-128K x batch 1-512")
     return ap.parse_args()
@@ -158,7 +161,7 @@ def run_ours(args, rank, world, local_rank):
     gen.manual_seed(1234 + (0 if args.mode == "tp" else rank))
     pages_per_req = (L + 63) // 64
     num_pages = B * pages_per_req
-    cache = ops.PagedMLACache(num_pages, dev)
+    cache = ops.PagedMLACacheBF16(num_pages, dev) if args.bf16 else ops.PagedMLACache(num_pages, dev)
     perm = torch.randperm(num_pages, generator=gen, device=dev).to(torch.int32)
     block_table = perm.view(B, pages_per_req).contiguous()
     # fill the cache with the product append kernel: every token is a one-token
@@ -186,7 +189,13 @@ def run_ours(args, rank, world, local_rank):
     ws = torch.empty(ops.mla_decode_workspace_bytes(B, rows), dtype=torch.uint8, device=dev)
     out = torch.empty((B, T, heads_local, 512) if T > 1 else (B, heads_local, 512), dtype=torch.bfloat16, device=dev)
     lse = torch.empty(out.shape[:-1], dtype=torch.float32, device=dev)
-    decode = ops.mla_decode_fp8_ex if T > 1 else ops.mla_decode_fp8
+    decode_fp8 = ops.mla_decode_fp8_ex if T > 1 else ops.mla_decode_fp8
+
+    def decode(qx):
+        if args.bf16:
+            ops.mla_decode_bf16(qx, cache.kv_c, cache.kv_rope, block_table, seq_lens, scale, ws)
+        else:
+            decode_fp8(qx, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
     gathered = torch.empty(world, B, heads_local, 512, dtype=torch.bfloat16, device=dev) if args.mode == "tp" else None
     del q_all
     torch.cuda.synchronize()
@@ -201,7 +210,7 @@ def run_ours(args, rank, world, local_rank):
             cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         if i is not None:
             ev_d0[i].record(stream)
-        decode(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        decode(q)
         if i is not None:
             ev_d1[i].record(stream)
         ops.mla_combine(ws, B, rows, out, lse)
@@ -240,7 +249,8 @@ def run_ours(args, rank, world, local_rank):
     ms_step = ms / args.steps
 
     peak, peak_src = measured_peaks()
-    kv_bytes = B * L * BYTES_PER_TOKEN
+    bytes_per_token = 2 * (512 + 64) if args.bf16 else BYTES_PER_TOKEN
+    kv_bytes = B * L * bytes_per_token
     dec_bytes = kv_bytes + B * rows * 576 * 2       # algorithmic bytes per decode launch
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9
     tokens_per_step = B * T * (world if args.mode == "dp" else 1)
@@ -264,7 +274,7 @@ def run_ours(args, rank, world, local_rank):
         for t in range(T - 1):
             cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         cache.append(c_d, r_d, block_table, seq_lens)
-        decode(q_d, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
+        decode(q_d)
         ops.mla_combine(ws, B, rows, out, lse)
         if gathered is not None:
             D.tp_gather_heads(out, gathered=gathered)
@@ -304,20 +314,20 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak" if args.mode == "dp" else "strong",
         "vs_baseline": None,
-        "dtype": "fp8e4m3 (f32 accumulate; bf16 RoPE)",
+        "dtype": "bf16 (NEXT-2 unquantized baseline; f32 accumulate)" if args.bf16 else "fp8e4m3 (f32 accumulate; bf16 RoPE)",
         "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
         "config": {
-            "workload": w["name"], "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
+            "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else ""), "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
             "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": T,
             "parallelism": f"{args.mode}{world}",
             "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
         },
         "roofline": {
-            "bound": "hbm", "kernel": "mla_decode_fp8 (plan + decode launches)",
+            "bound": "hbm", "kernel": ("mla_decode_bf16" if args.bf16 else "mla_decode_fp8") + " (plan + decode launches)",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(args.workload) if T == 1 else None, "peak_source": peak_src,
+            "traffic": ncu_traffic(args.workload) if T == 1 and not args.bf16 else None, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": dec_bytes, "decode_ms": round(dec_ms, 4),
-            "bytes_per_unit": f"{BYTES_PER_TOKEN} B per cached token + 1152 B per (request, query token, head) q row",
+            "bytes_per_unit": f"{bytes_per_token} B per cached token + 1152 B per (request, query token, head) q row",
         },
         "e2e": {"value": round(tokens_per_step / (e_ms / args.steps / 1e3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -508,7 +518,7 @@ def main():
             print(json.dumps(run_fetch(args, local_rank)))
         return
     res = run_ours(args, rank, world, local_rank)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick and not args.bf16:
         res["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(res))

@@ -170,6 +170,31 @@ mla_status mla_kv_fetch_dequant(const uint8_t* kv_fp8, const void* kv_rope, cons
                                 int64_t num_pages, int64_t total_rows, void* c_kv_out, void* k_pe_out,
                                 mla_stream_t stream);
 
+/*
+ * NEXT-2 baseline: the UNQUANTIZED BF16 MLA decode in the same
+ * kernel skeleton, for the paper's FP8-vs-BF16 comparison.
+ * It is not the method: no quantization anywhere; P (the softmax weights) is
+ * rounded to BF16 for the PV tensor-core product, as BF16 FlashMLA-style kernels do.
+ *
+ * mla_kv_append_bf16 -- copy the new token's latent into the BF16 paged pools
+ *   kv_c    bf16 [num_pages, page_size, 512]   (slot as in mla_kv_append_quant)
+ *   kv_rope bf16 [num_pages, page_size, 64]    (raw k_pe: no scale, no Eq.6 alignment)
+ *
+ * mla_decode_bf16 -- s_j = softmax_scale * (q . [c_kv_j | k_pe_j]) in fp32 (BF16 x BF16
+ * tensor-core products), online softmax per 64-token block, O <- gamma O + BF16(p) c_kv,
+ * split-KV partials in `workspace` exactly like mla_decode_fp8_ex (same q layout,
+ * q_len, row limits, workspace size and mla_combine / mla_combine_f32 follow-up).
+ * Pools must be 128-byte aligned; errors as for mla_decode_fp8_ex.
+ */
+mla_status mla_kv_append_bf16(const void* c_kv, const void* k_pe, const int32_t* block_table,
+                              const int32_t* seq_lens, int batch, int kv_lora_rank, int rope_dim, int page_size,
+                              int max_pages_per_seq, int64_t num_pages, void* kv_c, void* kv_rope,
+                              mla_stream_t stream);
+mla_status mla_decode_bf16(const void* q, const void* kv_c, const void* kv_rope, const int32_t* block_table,
+                           const int32_t* seq_lens, int batch, int num_heads, int q_len, int kv_lora_rank,
+                           int rope_dim, int page_size, int max_pages_per_seq, int64_t num_pages,
+                           float softmax_scale, void* workspace, size_t workspace_bytes, mla_stream_t stream);
+
 /* Same as mla_combine but writes fp32 output [batch, num_heads, kv_lora_rank]
  * (diagnostic: exposes the kernel result before the final BF16 rounding). */
 mla_status mla_combine_f32(const void* workspace, int batch, int num_heads, int kv_lora_rank, float* out,

@@ -99,3 +99,44 @@ extern "C" mla_status mla_kv_append_quant(const void* c_kv, const void* k_pe, co
       kv_fp8, (__nv_bfloat16*)kv_rope, kv_scale);
   return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
 }
+
+// NEXT-2 baseline: the unquantized BF16 cache of the same paged layout (content
+// [P, 64, 512] and RoPE [P, 64, 64] planes, no scales).  One warp per new token,
+// a straight 16-byte-vector copy into its paged slot.
+namespace snapmla {
+__global__ void __launch_bounds__(256) append_bf16_kernel(const uint4* __restrict__ c_kv, const uint4* __restrict__ k_pe,
+                                                          const int32_t* __restrict__ block_table,
+                                                          const int32_t* __restrict__ seq_lens, int batch,
+                                                          int max_pages, uint4* __restrict__ kv_c,
+                                                          uint4* __restrict__ kv_rope) {
+  const int lane = threadIdx.x & 31;
+  const int tok = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tok >= batch) return;
+  const int L = seq_lens[tok];
+  if (L <= 0) return;
+  const int pos = L - 1;
+  const int64_t slot = (int64_t)block_table[(int64_t)tok * max_pages + pos / kPage] * kPage + pos % kPage;
+  // 512 bf16 = 64 x 16 B: two vectors per lane; RoPE 64 bf16 = 8 vectors (lanes 0-7)
+  const uint4 a = __ldg(c_kv + (int64_t)tok * 64 + lane), b = __ldg(c_kv + (int64_t)tok * 64 + 32 + lane);
+  kv_c[slot * 64 + lane] = a;
+  kv_c[slot * 64 + 32 + lane] = b;
+  if (lane < 8) kv_rope[slot * 8 + lane] = __ldg(k_pe + (int64_t)tok * 8 + lane);
+}
+}  // namespace snapmla
+
+extern "C" mla_status mla_kv_append_bf16(const void* c_kv, const void* k_pe, const int32_t* block_table,
+                                         const int32_t* seq_lens, int batch, int kv_lora_rank, int rope_dim,
+                                         int page_size, int max_pages_per_seq, int64_t num_pages, void* kv_c,
+                                         void* kv_rope, mla_stream_t stream) {
+  if (batch < 0 || max_pages_per_seq < 0 || num_pages < 0) return MLA_ERR_SHAPE;
+  if (kv_lora_rank != kDc || rope_dim != kDr || page_size != kPage) return MLA_ERR_UNSUPPORTED;
+  if (batch == 0) return MLA_OK;
+  if (!c_kv || !k_pe || !block_table || !seq_lens || !kv_c || !kv_rope) return MLA_ERR_NULL;
+  if (max_pages_per_seq < 1) return MLA_ERR_SHAPE;
+  if (!aligned(c_kv, 16) || !aligned(k_pe, 16) || !aligned(kv_c, 16) || !aligned(kv_rope, 16)) return MLA_ERR_ALIGN;
+  const int warps = 8;
+  append_bf16_kernel<<<(batch + warps - 1) / warps, warps * 32, 0, (cudaStream_t)stream>>>(
+      (const uint4*)c_kv, (const uint4*)k_pe, block_table, seq_lens, batch, max_pages_per_seq, (uint4*)kv_c,
+      (uint4*)kv_rope);
+  return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}

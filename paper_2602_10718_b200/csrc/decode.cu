@@ -50,20 +50,15 @@ constexpr int kWarpSoftmax = 12;  // 12-15 softmax
 // register budget (setmaxnreg; balanced per SMSP: 2 acc + 1 issue + 1 softmax warp each):
 // 256 x 176 + 128 x 40 + 128 x 120 = 65,536 = 512 x 128 (launch)
 constexpr uint32_t kRegsAcc = 176, kRegsIssue = 40, kRegsSoftmax = 120;
-constexpr int kSlots = 5;         // KV ring depth (blocks)
 constexpr int kPSlots = 2;        // P' + stats ring depth (blocks)
 constexpr int kSSlots = 2;        // S ring depth (TMEM)
-constexpr int kTSlots = 3;        // TMEM ring of 64 x 256 PV half tiles
 constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
-constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024
+constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024 (FP8 KV slot)
 constexpr uint32_t kOffQr = 0;                              // [64 rows x 128 B] SW128 (q_r / sigma_q, BF16)
-constexpr uint32_t kOffP = 8192;                            // 2 slots x 4096 B, K-major core matrices
-constexpr uint32_t kOffKv = 16384;                          // 5 slots: 4 content boxes | RoPE box | scales
+constexpr uint32_t kOffP = 8192;                            // 2 P' slots (4 KB E4M3 / 8 KB BF16), K-major core matrices
 constexpr uint32_t kOffScaleHi = 5 * 8192 + 144;            // sigma_K of tokens 32-63 (bank-shifted by 16 B)
-constexpr uint32_t kOffBar = kOffKv + kSlots * kStage;
-constexpr uint32_t kSmemBytes = kOffBar + 4096 + 1024;      // barriers/stats + alignment slack
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+// KV slots, barrier region and SMEM size per variant: Variant<kBf> below
 static_assert(2 * 32 * kRegsAcc + 32 * kRegsIssue + 32 * kRegsSoftmax <= 4 * 32 * 128,
               "setmaxnreg budget per SMSP (launch: 4 warps x 128 registers)");
 
@@ -71,6 +66,8 @@ static_assert(2 * 32 * kRegsAcc + 32 * kRegsIssue + 32 * kRegsSoftmax <= 4 * 32 
 constexpr uint32_t kIdescQk8 = make_idesc(0, 0, 0, 0, 64, 64);      // E4M3 x E4M3, both K-major
 constexpr uint32_t kIdescQk16 = make_idesc(1, 1, 0, 0, 64, 64);     // BF16 x BF16
 constexpr uint32_t kIdescPv = make_idesc(0, 0, 0, 1, 64, 256);      // P' K-major, V MN-major
+constexpr uint32_t kIdescQkB = make_idesc(1, 1, 0, 0, 64, 64);      // BF16 variant: q content x K content
+constexpr uint32_t kIdescPvB = make_idesc(1, 1, 0, 1, 64, 256);     // BF16 variant: P K-major, V MN-major
 
 struct DecodeParams {
   const __nv_bfloat16* q;
@@ -106,10 +103,10 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
 #endif
 
 struct Bars {
-  uint64_t kv_full[kSlots], kv_empty[kSlots];   // TMA -> QK / PV_L + PV_R -> TMA
+  uint64_t kv_full[5], kv_empty[5];             // TMA -> QK / PV_L + PV_R -> TMA (max over variants)
   uint64_t s_full[kSSlots], s_empty[kSSlots];   // QK -> softmax / softmax -> QK
   uint64_t p_full[kPSlots], p_empty[kPSlots];   // P' + stats: softmax -> PV, acc / PV_L + PV_R + acc -> softmax
-  uint64_t t_full[kTSlots], t_free[kTSlots];    // T ring: PV -> WG / WG -> PV
+  uint64_t t_full[3], t_free[3];                // T ring: PV -> WG / WG -> PV
   uint64_t q_full, q_free;                      // Q-quant prologue -> QK / QK of a unit done -> prologue
   uint32_t tmem_base;
   float stat[kPSlots][3][64];         // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
@@ -284,17 +281,87 @@ __device__ __forceinline__ uint32_t t_slot_addr(uint32_t tmem, uint32_t s) {
   return tmem + (s == 0 ? 256u : (16u << 16) + 256u * (s - 1));
 }
 
+// Per-variant layout: FP8 (the method) and the BF16 baseline variant (NEXT-2, same skeleton,
+// unquantized cache / Q / P).  BF16: 8 content boxes + RoPE = 72 KB per block (two slots fit),
+// q content (1 KB per row) in TMEM columns 128-383 of lanes 0-15, so only the two T half-slots
+// of lanes 16-31 remain; P' is BF16 (8 KB per slot).
+template <bool kBf> struct Variant;
+template <> struct Variant<false> {
+  static constexpr int kSlots = 5, kTSlots = 3, kBoxes = 4;
+  static constexpr uint32_t kTx = kKvTx, kStage = 41984, kPBytes = 4096, kOffKv = 16384;
+  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 4096 + 1024;
+  static __device__ __forceinline__ uint32_t t_slot(uint32_t tmem, uint32_t s) { return t_slot_addr(tmem, s); }
+};
+template <> struct Variant<true> {
+  static constexpr int kSlots = 2, kTSlots = 2, kBoxes = 8;
+  static constexpr uint32_t kTx = 9 * kBoxBytes, kStage = 9 * kBoxBytes, kPBytes = 8192, kOffKv = 8192 + 2 * 8192;
+  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 4096 + 1024;
+  static __device__ __forceinline__ uint32_t t_slot(uint32_t tmem, uint32_t s) {
+    return tmem + (16u << 16) + 256u * s;
+  }
+};
+static_assert(Variant<false>::kSmem <= 232448 && Variant<true>::kSmem <= 232448, "shared memory budget");
+
+// BF16 variant QK: 32 x kind::f16 (K = 16) over the content (A = q in TMEM, columns tQ + 8 kk)
+// + 4 x kind::f16 over the RoPE, one accumulator; commit to `bar`.
+#define SNAPMLA_QKB(ta, bo, acc)                                                               \
+  "add.u32 t, %1, " #ta ";\n\tadd.s64 b, %2, " #bo ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], b, %3, " acc ";\n\t"
+__device__ __forceinline__ void qk_issue_bf16(uint32_t dS, uint32_t tQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
+                                              uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, t;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      SNAPMLA_QKB(0, 0, "pf") SNAPMLA_QKB(8, 2, "pt") SNAPMLA_QKB(16, 4, "pt") SNAPMLA_QKB(24, 6, "pt")
+      SNAPMLA_QKB(32, 512, "pt") SNAPMLA_QKB(40, 514, "pt") SNAPMLA_QKB(48, 516, "pt") SNAPMLA_QKB(56, 518, "pt")
+      SNAPMLA_QKB(64, 1024, "pt") SNAPMLA_QKB(72, 1026, "pt") SNAPMLA_QKB(80, 1028, "pt") SNAPMLA_QKB(88, 1030, "pt")
+      SNAPMLA_QKB(96, 1536, "pt") SNAPMLA_QKB(104, 1538, "pt") SNAPMLA_QKB(112, 1540, "pt") SNAPMLA_QKB(120, 1542, "pt")
+      SNAPMLA_QKB(128, 2048, "pt") SNAPMLA_QKB(136, 2050, "pt") SNAPMLA_QKB(144, 2052, "pt") SNAPMLA_QKB(152, 2054, "pt")
+      SNAPMLA_QKB(160, 2560, "pt") SNAPMLA_QKB(168, 2562, "pt") SNAPMLA_QKB(176, 2564, "pt") SNAPMLA_QKB(184, 2566, "pt")
+      SNAPMLA_QKB(192, 3072, "pt") SNAPMLA_QKB(200, 3074, "pt") SNAPMLA_QKB(208, 3076, "pt") SNAPMLA_QKB(216, 3078, "pt")
+      SNAPMLA_QKB(224, 3584, "pt") SNAPMLA_QKB(232, 3586, "pt") SNAPMLA_QKB(240, 3588, "pt") SNAPMLA_QKB(248, 3590, "pt")
+      SNAPMLA_QK16(0) SNAPMLA_QK16(2) SNAPMLA_QK16(4) SNAPMLA_QK16(6)
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}"
+      ::"r"(dS), "r"(tQ), "l"(dK), "r"(kIdescQkB), "l"(dQr), "l"(dKr), "r"(kIdescQk16), "r"(bar)
+      : "memory");
+}
+
+// BF16 variant PV half: T = P (64 x 64 tokens, BF16 K-major) x V (64 tokens x 256 dims, BF16
+// MN-major, 4 boxes of 64 dims), 4 x kind::f16 (K = 16: +2048 B in both operands per step).
+__device__ __forceinline__ void pv_issue_bf16(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t, uint32_t bar_p,
+                                              uint32_t bar_kv) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, 256;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, 384;\n\tadd.s64 b, %2, 384;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPvB), "r"(bar_t), "r"(bar_p), "r"(bar_kv)
+      : "memory");
+}
+
+template <bool kBf>
 __global__ void __launch_bounds__(kThreads, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
                       const DecodeParams p) {
+  using V = Variant<kBf>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar0 = sbase + kOffBar;
+  const uint32_t bar0 = sbase + V::kOffBar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- setup overlaps the plan kernel (programmatic dependent launch)
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSlots; ++i) {
+    for (int i = 0; i < V::kSlots; ++i) {
       mbar_init(BAR(kv_full) + 8 * i, 1);
       mbar_init(BAR(kv_empty) + 8 * i, 2);
     }
@@ -306,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(BAR(s_full) + 8 * i, 1);
       mbar_init(BAR(s_empty) + 8 * i, 4);
     }
-    for (int i = 0; i < kTSlots; ++i) {
+    for (int i = 0; i < V::kTSlots; ++i) {
       mbar_init(BAR(t_full) + 8 * i, 1);
       mbar_init(BAR(t_free) + 8 * i, 4);
     }
@@ -353,18 +420,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (it.next(u)) {
           const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
           for (int j = u.k0; j < u.k1; ++j, ++n) {
-            const uint32_t st = n % kSlots;
-            mbar_wait_backoff(BAR(kv_empty) + 8 * st, ((n / kSlots) & 1) ^ 1);
+            const uint32_t st = n % V::kSlots;
+            mbar_wait_backoff(BAR(kv_empty) + 8 * st, ((n / V::kSlots) & 1) ^ 1);
             TRACE(TR_TMA, n);
             const int row = __ldg(bt + j) * kPage;
-            const uint32_t dst = sbase + kOffKv + st * kStage;
+            const uint32_t dst = sbase + V::kOffKv + st * V::kStage;
             const uint32_t full = BAR(kv_full) + 8 * st;
-            mbar_arrive_expect_tx(full, kKvTx);
+            mbar_arrive_expect_tx(full, V::kTx);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * kBoxBytes, &tm_kv, full, c * 128, row, pol);
-            tma_load_2d(dst + 4 * kBoxBytes, &tm_rope, full, 0, row, pol);
-            bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 128, full, pol);
-            bulk_load(dst + kOffScaleHi, p.kv_scale + (int64_t)row + 32, 128, full, pol);
+            for (int c = 0; c < V::kBoxes; ++c)   // content boxes of 128 B (128 E4M3 / 64 BF16 values) x 64 tokens
+              tma_load_2d(dst + c * kBoxBytes, &tm_kv, full, c * (kBf ? 64 : 128), row, pol);
+            tma_load_2d(dst + V::kBoxes * kBoxBytes, &tm_rope, full, 0, row, pol);
+            if constexpr (!kBf) {
+              bulk_load(dst + 5 * kBoxBytes, p.kv_scale + (int64_t)row, 128, full, pol);
+              bulk_load(dst + kOffScaleHi, p.kv_scale + (int64_t)row + 32, 128, full, pol);
+            }
           }
         }
       }
@@ -375,14 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (it.next(u)) {
         mbar_wait(BAR(q_full), unit & 1, 2, unit);
         for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kSlots, ss = n % kSSlots;
-          mbar_wait(BAR(kv_full) + 8 * st, (n / kSlots) & 1, 3, n);
+          const uint32_t st = n % V::kSlots, ss = n % kSSlots;
+          mbar_wait(BAR(kv_full) + 8 * st, (n / V::kSlots) & 1, 3, n);
           mbar_wait(BAR(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
           tc_fence_after();
           if (lane == 0) TRACE(TR_QK, n);
-          const uint32_t kv = sbase + kOffKv + st * kStage;
-          qk_issue(tmem_S + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
-                   make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
+          const uint32_t kv = sbase + V::kOffKv + st * V::kStage;
+          if constexpr (kBf)
+            qk_issue_bf16(tmem_S + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                          make_smem_desc(kv + 8 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
+          else
+            qk_issue(tmem_S + 64 * ss, tmem + kTmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                     make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), BAR(s_full) + 8 * ss);
         }
         mma_commit_ws(BAR(q_free));   // Q (TMEM + SMEM) reusable once this unit's QK MMAs completed
         ++unit;
@@ -393,17 +467,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t n = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % kSlots, ps = n % kPSlots;
-          const uint32_t h = 2 * n + half, ts = h % kTSlots;
+          const uint32_t st = n % V::kSlots, ps = n % kPSlots;
+          const uint32_t h = 2 * n + half, ts = h % V::kTSlots;
           mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);                  // P'(n) in SMEM
-          if (h >= kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / kTSlots - 1) & 1, 6, n);   // slot read
+          if (h >= V::kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / V::kTSlots - 1) & 1, 6, n);   // slot read
           tc_fence_after();
           if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
-          const uint32_t pA = sbase + kOffP + ps * 4096;
-          const uint32_t vb = sbase + kOffKv + st * kStage + (2 * half) * kBoxBytes;
-          pv_issue(t_slot_addr(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
-                   make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
-                   BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
+          const uint32_t pA = sbase + kOffP + ps * V::kPBytes;
+          const uint32_t vb = sbase + V::kOffKv + st * V::kStage + (V::kBoxes / 2 * half) * kBoxBytes;
+          if constexpr (kBf)
+            pv_issue_bf16(V::t_slot(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                          make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
+                          BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
+          else
+            pv_issue(V::t_slot(tmem, ts), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                     make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), BAR(t_full) + 8 * ts,
+                     BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
         }
       }
     }
@@ -423,7 +502,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh
       if (unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // QK of the previous unit done
       float c_row;
-      {
+      if constexpr (kBf) {
+        // BF16 variant (NEXT-2): the unquantized q row goes to TMEM / SMEM as is; c = scale * log2(e)
+        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
+        c_row = p.scale_log2;
+        // content elements [256 hh, 256 hh + 256) = TMEM columns kTmemQ + 128 hh + [0, 128), 2 per column
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t qa[32];
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            const uint4 v = row_ok ? __ldg(qrow + 32 * hh + 8 * i + g8) : make_uint4(0, 0, 0, 0);
+            qa[4 * g8] = v.x;
+            qa[4 * g8 + 1] = v.y;
+            qa[4 * g8 + 2] = v.z;
+            qa[4 * g8 + 3] = v.w;
+          }
+          tmem_st_16x32bx2_x32<128>(tmem + lane_off + kTmemQ + 32 * i, qa);
+        }
+        tmem_wait_st();
+#pragma unroll
+        for (int gch = 0; gch < 4; ++gch) {
+          const int c = 4 * hh + gch;
+          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
+          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(q_full));
+      } else {
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
         float amax = 0.f;
 #pragma unroll
@@ -495,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // block n's P' / stats stores, fence and arrive, which hide its latency.
       float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % kSlots, ss = n % kSSlots, ps = n % kPSlots;
+        const uint32_t st = n % V::kSlots, ss = n % kSSlots, ps = n % kPSlots;
         if (j == u.k0) {
           mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
           tc_fence_after();
@@ -508,13 +616,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(BAR(s_empty) + 8 * ss);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
         // sigma_K of my 32 tokens (from the TMA'd slot)
-        const uint32_t sk = sbase + kOffKv + st * kStage + (hh ? kOffScaleHi : 5 * kBoxBytes);
+        const uint32_t sk = sbase + V::kOffKv + st * V::kStage + (hh ? kOffScaleHi : 5 * kBoxBytes);
         const int nvalid = L - (j * kBc + 32 * hh);   // tokens of my half inside the sequence
         float4 skv[8];                                                 // sigma_K of my 32 tokens, kept
 #pragma unroll
-        for (int e = 0; e < 8; ++e) skv[e] = lds_f4(sk + 16 * e);
+        for (int e = 0; e < 8; ++e) skv[e] = kBf ? make_float4(1.f, 1.f, 1.f, 1.f) : lds_f4(sk + 16 * e);
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {                              // Alg.1 step 3 (descale)
+          if constexpr (kBf) break;
           const float4 s4 = skv[e / 4];
           const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4.x, s4.y));
           const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4.z, s4.w));
@@ -546,8 +655,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
           const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));   // step 5 (block reference)
           const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
-          const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));           // step 6: p * sigma_K
-          const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
+          const float2 w0 = kBf ? p0 : __fmul2_rn(p0, make_float2(s4.x, s4.y));   // step 6: p * sigma_K
+          const float2 w1 = kBf ? p1 : __fmul2_rn(p1, make_float2(s4.z, s4.w));
           ls0 = __fadd2_rn(ls0, p0);
           ls1 = __fadd2_rn(ls1, p1);
           tt[e] = w0.x;
@@ -564,15 +673,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
         // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
         // P' = 0 and is skipped by the recurrence (R11)
-        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
+        // BF16 variant: P = BF16(p) with sigma_p = 1 (no P quantization)
+        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = kBf ? 1.f : __fdiv_rn(mb, 448.0f);
         const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
         const float2 inv2 = make_float2(inv, inv);
-        uint32_t pw[8];
+        uint32_t pw[kBf ? 16 : 8];
+        if constexpr (kBf) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
-          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
-          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+          for (int e = 0; e < 16; ++e) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(tt[2 * e], tt[2 * e + 1]);
+            pw[e] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
+            const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
+            pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+          }
         }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
         if (j + 1 < u.k1) {   // prefetch S(n+1)
@@ -585,16 +703,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         // eight accumulator warps read its stats
         mbar_wait(BAR(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, n);
-        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
+        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16 (E4M3);
+        // BF16: (tok/8)*1024 + row*16 + 2 (tok%8)
         if (hh == 0) {
           const uint32_t sa = stat0 + ps * (3 * 64 * 4);
           sts_f32(sa, st_m);
           sts_f32(sa + 256, st_sig);
           sts_f32(sa + 512, lsum);
         }
-        const uint32_t pdst = sbase + kOffP + ps * 4096 + r * 16;
-        sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
-        sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        const uint32_t pdst = sbase + kOffP + ps * V::kPBytes + r * 16;
+        if constexpr (kBf) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sts_u4(pdst + (4 * hh + c) * 1024, pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+        } else {
+          sts_u4(pdst + (2 * hh) * 1024, pw[0], pw[1], pw[2], pw[3]);
+          sts_u4(pdst + (2 * hh + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_C2, n);
         fence_proxy_async_smem();
         __syncwarp();
@@ -649,11 +773,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_O = mb;
           sig_O = sb;
         }
-        const uint32_t h = 2 * n + w, ts = h % kTSlots;
-        mbar_wait(BAR(t_full) + 8 * ts, (h / kTSlots) & 1, 10, n);      // T half = P'(n) V complete
+        const uint32_t h = 2 * n + w, ts = h % V::kTSlots;
+        mbar_wait(BAR(t_full) + 8 * ts, (h / V::kTSlots) & 1, 10, n);      // T half = P'(n) V complete
         tc_fence_after();
         if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
-        const uint32_t taddr = t_slot_addr(tmem, ts) + lane_off;
+        const uint32_t taddr = V::t_slot(tmem, ts) + lane_off;
         const float2 g2 = make_float2(gamma, gamma);
         // software-pipelined T reads (8 chunks of 16 columns)
         uint32_t tv[2][16];
@@ -1364,11 +1488,11 @@ extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_s
   return ws_layout(batch, num_heads, num_sms).total;
 }
 
-extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* kv_rope,
-                                        const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
-                                        int batch, int num_heads, int q_len, int kv_lora_rank, int rope_dim,
-                                        int page_size, int max_pages_per_seq, int64_t num_pages, float softmax_scale,
-                                        void* workspace, size_t workspace_bytes, mla_stream_t stream) {
+static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, const void* kv_rope,
+                                const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
+                                int batch, int num_heads, int q_len, int kv_lora_rank, int rope_dim,
+                                int page_size, int max_pages_per_seq, int64_t num_pages, float softmax_scale,
+                                void* workspace, size_t workspace_bytes, mla_stream_t stream) {
   if (batch < 0 || num_heads <= 0 || q_len <= 0 || max_pages_per_seq < 0 || num_pages < 0) return MLA_ERR_SHAPE;
   if (kv_lora_rank != kDc || rope_dim != kDr || page_size != kPage) return MLA_ERR_UNSUPPORTED;
   const int heads = num_heads;
@@ -1377,8 +1501,8 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   if (num_pages * kPage >= (int64_t)INT32_MAX) return MLA_ERR_UNSUPPORTED;   // TMA row coordinate is int32
   if (!workspace) return MLA_ERR_WORKSPACE;
   if (batch == 0) return MLA_OK;
-  if (!q || !kv_fp8 || !kv_rope || !kv_scale || !block_table || !seq_lens) return MLA_ERR_NULL;
-  if (!aligned(q, 16) || !aligned(kv_fp8, 128) || !aligned(kv_rope, 128) || !aligned(kv_scale, 16) ||
+  if (!q || !kv_fp8 || !kv_rope || (!bf16 && !kv_scale) || !block_table || !seq_lens) return MLA_ERR_NULL;
+  if (!aligned(q, 16) || !aligned(kv_fp8, 128) || !aligned(kv_rope, 128) || (!bf16 && !aligned(kv_scale, 16)) ||
       !aligned(workspace, 256))
     return MLA_ERR_ALIGN;
   const int sms = device_num_sms();
@@ -1386,7 +1510,7 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   if (workspace_bytes < wl.total) return MLA_ERR_WORKSPACE;
   const int n_ht = (num_heads + kHeadTile - 1) / kHeadTile;
-  const bool pair = n_ht == 2 && g_pair;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
+  const bool pair = !bf16 && n_ht == 2 && g_pair;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
   int groups = sms / n_ht;
   if (pair) {
     static int max_clusters = -1;
@@ -1410,7 +1534,9 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   CUtensorMap tm_kv, tm_rope;
   const uint64_t rows = (uint64_t)num_pages * kPage;
   if (num_pages == 0) return MLA_ERR_SHAPE;
-  if (!encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 64)) return MLA_ERR_CUDA;
+  if (bf16 ? !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_fp8, kDc, rows, kDc * 2, 64, 64)
+           : !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 64))
+    return MLA_ERR_CUDA;
   if (!encode_2d(&tm_rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_rope, kDr, rows, kDr * 2, 64, 64))
     return MLA_ERR_CUDA;
 
@@ -1422,12 +1548,13 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   plan_kernel<<<1, 1024, 0, st>>>(seq_lens, batch, num_heads, groups, hdr, cum, first);
   if (cudaGetLastError() != cudaSuccess) return MLA_ERR_CUDA;
 
-  if (!pair && cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-      cudaSuccess)
+  const uint32_t smem = pair ? kPSmemBytes : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
+  if (!pair && cudaFuncSetAttribute(bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return MLA_ERR_CUDA;
   DecodeParams prm;
   prm.q = (const __nv_bfloat16*)q;
-  prm.kv_fp8 = kv_fp8;
+  prm.kv_fp8 = static_cast<const uint8_t*>(kv_fp8);
   prm.kv_rope = (const __nv_bfloat16*)kv_rope;
   prm.kv_scale = kv_scale;
   prm.block_table = block_table;
@@ -1451,7 +1578,7 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * n_ht);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = pair ? kPSmemBytes : kSmemBytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1460,10 +1587,31 @@ extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, co
   cfg.numAttrs = 1;
   if (pair) {
     if (cudaLaunchKernelEx(&cfg, mla_decode_pair_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
-  } else if (cudaLaunchKernelEx(&cfg, mla_decode_kernel, tm_kv, tm_rope, prm) != cudaSuccess) {
+  } else if (cudaLaunchKernelEx(&cfg, bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>, tm_kv, tm_rope,
+                                prm) != cudaSuccess) {
     return MLA_ERR_CUDA;
   }
   return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}
+
+extern "C" mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* kv_rope,
+                                        const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
+                                        int batch, int num_heads, int q_len, int kv_lora_rank, int rope_dim,
+                                        int page_size, int max_pages_per_seq, int64_t num_pages, float softmax_scale,
+                                        void* workspace, size_t workspace_bytes, mla_stream_t stream) {
+  return decode_launch(false, q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, batch, num_heads, q_len,
+                       kv_lora_rank, rope_dim, page_size, max_pages_per_seq, num_pages, softmax_scale, workspace,
+                       workspace_bytes, stream);
+}
+
+extern "C" mla_status mla_decode_bf16(const void* q, const void* kv_c, const void* kv_rope,
+                                      const int32_t* block_table, const int32_t* seq_lens, int batch, int num_heads,
+                                      int q_len, int kv_lora_rank, int rope_dim, int page_size,
+                                      int max_pages_per_seq, int64_t num_pages, float softmax_scale, void* workspace,
+                                      size_t workspace_bytes, mla_stream_t stream) {
+  return decode_launch(true, q, kv_c, kv_rope, nullptr, block_table, seq_lens, batch, num_heads, q_len,
+                       kv_lora_rank, rope_dim, page_size, max_pages_per_seq, num_pages, softmax_scale, workspace,
+                       workspace_bytes, stream);
 }
 
 extern "C" mla_status mla_decode_fp8(const void* q, const uint8_t* kv_fp8, const void* kv_rope,

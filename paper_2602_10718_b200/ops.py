@@ -4,7 +4,8 @@ device memory and the current stream; nothing else of torch is used.
 
 Same names as the C ABI (include/snapmla.h):
   mla_kv_append_quant, mla_decode_workspace_bytes, mla_decode_fp8,
-  mla_decode_fp8_ex, mla_combine, mla_combine_f32, mla_kv_fetch_dequant
+  mla_decode_fp8_ex, mla_combine, mla_combine_f32, mla_kv_fetch_dequant,
+  mla_kv_append_bf16, mla_decode_bf16 (NEXT-2: the unquantized BF16 baseline in the same skeleton)
 There is no CPU fallback: a missing library or a non-CUDA tensor raises.
 """
 import ctypes
@@ -52,6 +53,10 @@ def lib():
     L.mla_combine.argtypes = [_P, _I, _I, _I, _P, _P, _P]
     L.mla_combine_f32.restype = _I
     L.mla_combine_f32.argtypes = [_P, _I, _I, _I, _P, _P, _P]
+    L.mla_kv_append_bf16.restype = _I
+    L.mla_kv_append_bf16.argtypes = [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _P, _P, _P]
+    L.mla_decode_bf16.restype = _I
+    L.mla_decode_bf16.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
     if os.environ.get("SNAPMLA_PAIR") == "1":   # experimental CTA-pair kernel (include/snapmla_debug.h)
         L.mla_debug_set_pair(1)
     if os.environ.get("SNAPMLA_PAIR_GROUPS"):
@@ -62,7 +67,8 @@ def lib():
 
 def exported_symbols():
     return ["mla_status_str", "mla_abi_version", "mla_kv_append_quant", "mla_decode_workspace_bytes",
-            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant"]
+            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant",
+            "mla_kv_append_bf16", "mla_decode_bf16"]
 
 
 def _check(status, what):
@@ -156,6 +162,41 @@ def mla_kv_fetch_dequant(kv_fp8, kv_rope, kv_scale, block_table, tok_start, out_
     return c_kv_out, k_pe_out
 
 
+def mla_kv_append_bf16(c_kv, k_pe, block_table, seq_lens, kv_c, kv_rope, stream=None):
+    """NEXT-2 baseline: copy one token per request into the unquantized BF16 paged pools."""
+    batch = c_kv.shape[0]
+    _check(lib().mla_kv_append_bf16(
+        _dev(c_kv, torch.bfloat16, "c_kv"), _dev(k_pe, torch.bfloat16, "k_pe"),
+        _dev(block_table, torch.int32, "block_table"), _dev(seq_lens, torch.int32, "seq_lens"),
+        batch, c_kv.shape[1], k_pe.shape[1], kv_c.shape[1], block_table.shape[1], kv_c.shape[0],
+        _dev(kv_c, torch.bfloat16, "kv_c"), _dev(kv_rope, torch.bfloat16, "kv_rope"), _stream(stream)),
+        "mla_kv_append_bf16")
+
+
+def mla_decode_bf16(q, kv_c, kv_rope, block_table, seq_lens, softmax_scale, workspace, stream=None):
+    """NEXT-2 baseline decode: q bf16 [batch, num_heads, 576] or [batch, q_len, num_heads, 576]."""
+    batch = q.shape[0]
+    q_len, num_heads = (q.shape[1], q.shape[2]) if q.dim() == 4 else (1, q.shape[1])
+    _check(lib().mla_decode_bf16(
+        _dev(q, torch.bfloat16, "q"), _dev(kv_c, torch.bfloat16, "kv_c"), _dev(kv_rope, torch.bfloat16, "kv_rope"),
+        _dev(block_table, torch.int32, "block_table"), _dev(seq_lens, torch.int32, "seq_lens"),
+        batch, num_heads, q_len, D_C, D_R, kv_c.shape[1], block_table.shape[1], kv_c.shape[0],
+        float(softmax_scale), _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream)), "mla_decode_bf16")
+
+
+class PagedMLACacheBF16:
+    """NEXT-2 baseline: unquantized paged cache, kv_c bf16 [P,64,512], kv_rope bf16 [P,64,64] (1152 B / token)."""
+
+    def __init__(self, num_pages, device="cuda"):
+        self.num_pages = int(num_pages)
+        self.kv_c = torch.zeros(num_pages, PAGE, D_C, dtype=torch.bfloat16, device=device)
+        self.kv_rope = torch.zeros(num_pages, PAGE, D_R, dtype=torch.bfloat16, device=device)
+
+    def append(self, c_kv, k_pe, block_table, seq_lens, stream=None):
+        mla_kv_append_bf16(c_kv, k_pe, block_table, seq_lens, self.kv_c, self.kv_rope, stream)
+
+
 class PagedMLACache:
     """Device-resident paged FP8 latent cache (three planes sharing one slot index):
     kv_fp8 u8 [P,64,512] E4M3 codes, kv_rope bf16 [P,64,64] = k_pe/sigma, kv_scale f32 [P,64].
@@ -173,7 +214,8 @@ class PagedMLACache:
 
 def decode_step(q, cache, block_table, seq_lens, softmax_scale, workspace=None, out=None, lse=None,
                 stream=None, f32_out=False):
-    """mla_decode_fp8 (q [B, H, 576]) or mla_decode_fp8_ex (q [B, q_len, H, 576], MTP) + mla_combine.
+    """mla_decode_fp8 (q [B, H, 576]) or mla_decode_fp8_ex (q [B, q_len, H, 576], MTP) + mla_combine;
+    mla_decode_bf16 when `cache` is a PagedMLACacheBF16 (NEXT-2 baseline).
     Returns (out, lse) shaped like q's leading dims."""
     lead = tuple(q.shape[:-1])
     batch, rows = q.shape[0], 1
@@ -185,7 +227,9 @@ def decode_step(q, cache, block_table, seq_lens, softmax_scale, workspace=None, 
         out = torch.empty(lead + (D_C,), dtype=torch.float32 if f32_out else torch.bfloat16, device=q.device)
     if lse is None:
         lse = torch.empty(lead, dtype=torch.float32, device=q.device)
-    if q.dim() == 4:
+    if isinstance(cache, PagedMLACacheBF16):
+        mla_decode_bf16(q, cache.kv_c, cache.kv_rope, block_table, seq_lens, softmax_scale, workspace, stream)
+    elif q.dim() == 4:
         mla_decode_fp8_ex(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,
                           workspace, stream)
     else:

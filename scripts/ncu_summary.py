@@ -113,7 +113,7 @@ def main():
             for k, (v, f) in shares.items():
                 lines.append(f"{k[:80]:80s} {v:.6e} {100 * f:5.1f}%")
             entry["decode_share_of_step_ncu"] = next((f for k, (v, f) in shares.items() if "mla_decode_kernel" in k), None)
-        summary[w] = entry
+        summary[w + ("_bf16" if "bf16" in tag else "")] = entry   # the BF16 baseline keeps its own key
         open(os.path.join(PROF, f"{tag}_ncu_{w}.txt"), "w").write("\n".join(lines) + "\n")
         print(w, json.dumps(entry))
     json.dump(summary, open(sp, "w"), indent=1)
