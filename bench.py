@@ -52,7 +52,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="override per-rank batch")
     ap.add_argument("--context", type=int, default=None)
     ap.add_argument("--heads", type=int, default=None)
-    ap.add_argument("--mode", default="dp", choices=["dp", "tp"])
+    ap.add_argument("--mode", default="dp", choices=["dp", "tp", "dptp"])
+    ap.add_argument("--tp", type=int, default=2, help="--mode dptp: TP group size (world = DP x TP)")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="tp / dptp: all-gather fused into the combine epilogue (mla_combine_gather, symmetric memory)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--quick", action="store_true",
@@ -152,13 +155,22 @@ def run_ours(args, rank, world, local_rank):
     w = workload(args)
     B, H, L = w["batch"], w["heads"], w["context"]
     T = args.mtp
-    head0, head1 = D.tp_range(H, world, rank) if args.mode == "tp" else (0, H)
+    # head partition: TP over the whole world, or over consecutive-rank TP groups (DP x TP)
+    tp_world, t_idx, d_idx, tp_group = 1, 0, rank, None
+    if args.mode == "tp":
+        tp_world, t_idx, d_idx = world, rank, 0
+    elif args.mode == "dptp":
+        tp_world = args.tp
+        d_idx, t_idx = D.dptp_coords(world, tp_world, rank)
+        tp_group = D.dptp_groups(world, tp_world) if world > 1 else None
+    n_dp = world // tp_world
+    head0, head1 = D.tp_range(H, tp_world, t_idx)
     heads_local = head1 - head0
     scale = synth.DEFAULT_SOFTMAX_SCALE
 
     gen = torch.Generator(device=dev)
     # TP replicas hold identical KV; DP ranks hold their own requests
-    gen.manual_seed(1234 + (0 if args.mode == "tp" else rank))
+    gen.manual_seed(1234 + d_idx)   # the ranks of one TP group hold identical KV
     pages_per_req = (L + 63) // 64
     num_pages = B * pages_per_req
     cache = ops.PagedMLACacheBF16(num_pages, dev) if args.bf16 else ops.PagedMLACache(num_pages, dev)
@@ -196,7 +208,25 @@ def run_ours(args, rank, world, local_rank):
             ops.mla_decode_bf16(qx, cache.kv_c, cache.kv_rope, block_table, seq_lens, scale, ws)
         else:
             decode_fp8(qx, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
-    gathered = torch.empty(world, B, heads_local, 512, dtype=torch.bfloat16, device=dev) if args.mode == "tp" else None
+    gathered, peer_ptrs = None, None
+    if tp_world > 1 and args.fused_gather:
+        if T > 1:
+            raise SystemExit("--fused-gather supports mtp = 1")
+        gathered, peer_ptrs = D.symmetric_gather_output((B, H, 512), tp_group or dist.group.WORLD, dev)
+    elif tp_world > 1:
+        gathered = torch.empty(tp_world, B, heads_local, 512, dtype=torch.bfloat16, device=dev)
+
+    if peer_ptrs is not None:
+        out = gathered[:, head0:head1]   # this rank's heads of the gathered result (e2e read-back)
+
+    def combine_and_gather():
+        if peer_ptrs is not None:   # NEXT-4(c): peer stores from the combine epilogue + stream barrier
+            ops.mla_combine_gather(ws, B, rows, peer_ptrs, t_idx, lse)
+            D.stream_barrier(tp_group, dev)
+            return
+        ops.mla_combine(ws, B, rows, out, lse)
+        if gathered is not None:
+            D.tp_gather_heads(out, group=tp_group, gathered=gathered)
     del q_all
     torch.cuda.synchronize()
 
@@ -213,9 +243,7 @@ def run_ours(args, rank, world, local_rank):
         decode(q)
         if i is not None:
             ev_d1[i].record(stream)
-        ops.mla_combine(ws, B, rows, out, lse)
-        if gathered is not None:
-            D.tp_gather_heads(out, gathered=gathered)
+        combine_and_gather()
 
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -253,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
     kv_bytes = B * L * bytes_per_token
     dec_bytes = kv_bytes + B * rows * 576 * 2       # algorithmic bytes per decode launch
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9
-    tokens_per_step = B * T * (world if args.mode == "dp" else 1)
+    tokens_per_step = B * T * n_dp
     if args.quick:
         return {"metric": METRIC, "value": round(tokens_per_step / (ms_step / 1e3), 1),
                 "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True,
@@ -275,9 +303,7 @@ def run_ours(args, rank, world, local_rank):
             cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         cache.append(c_d, r_d, block_table, seq_lens)
         decode(q_d)
-        ops.mla_combine(ws, B, rows, out, lse)
-        if gathered is not None:
-            D.tp_gather_heads(out, gathered=gathered)
+        combine_and_gather()
         out_h.copy_(out, non_blocking=True)
         lse_h.copy_(lse, non_blocking=True)
 
@@ -312,14 +338,14 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak" if args.mode == "dp" else "strong",
+        "scaling": "strong" if args.mode == "tp" else "weak",
         "vs_baseline": None,
         "dtype": "bf16 (NEXT-2 unquantized baseline; f32 accumulate)" if args.bf16 else "fp8e4m3 (f32 accumulate; bf16 RoPE)",
         "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
         "config": {
             "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else ""), "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
             "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": T,
-            "parallelism": f"{args.mode}{world}",
+            "parallelism": f"dp{n_dp}tp{tp_world}" + ("+fused-gather" if peer_ptrs is not None else ""),
             "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
         },
         "roofline": {

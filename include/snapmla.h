@@ -195,6 +195,21 @@ mla_status mla_decode_bf16(const void* q, const void* kv_c, const void* kv_rope,
                            int rope_dim, int page_size, int max_pages_per_seq, int64_t num_pages,
                            float softmax_scale, void* workspace, size_t workspace_bytes, mla_stream_t stream);
 
+/*
+ * mla_combine_gather -- NEXT-4(c): mla_combine with the tensor-parallel all-gather fused
+ * into its epilogue.  With heads partitioned over `world` ranks (rank r decoded heads
+ * [r * num_heads, (r + 1) * num_heads) into `workspace`), every rank's combined BF16 rows
+ * are stored straight into ALL ranks' gathered outputs:
+ *   out_peers[i]  bf16 [batch, world * num_heads, 512] on rank i (host array of `world`
+ *                 device pointers, peer-mapped, e.g. CUDA IPC / symmetric memory over
+ *                 NVLink; world <= 8); rank r writes rows r * num_heads + h.
+ *   lse           fp32 [batch, num_heads] of this rank's heads (local), may be NULL.
+ * The stores are plain P2P writes: the caller orders them before any consumer on another
+ * rank with a stream-ordered barrier (e.g. a one-element NCCL all-reduce) after this call.
+ */
+mla_status mla_combine_gather(const void* workspace, int batch, int num_heads, int kv_lora_rank,
+                              void* const* out_peers, int world, int rank, float* lse, mla_stream_t stream);
+
 /* Same as mla_combine but writes fp32 output [batch, num_heads, kv_lora_rank]
  * (diagnostic: exposes the kernel result before the final BF16 rounding). */
 mla_status mla_combine_f32(const void* workspace, int batch, int num_heads, int kv_lora_rank, float* out,

@@ -7,10 +7,21 @@
 
 namespace snapmla {
 
-template <bool kF32Out>
+// NEXT-4(c): the TP all-gather fused into the combine epilogue.  Each rank combines its
+// head slice and stores the BF16 rows straight into EVERY rank's gathered output
+// [batch, world * num_heads, 512] (heads rank-major) through peer-mapped pointers
+// (NVLink P2P stores; on one GPU the "peers" are local buffers).
+constexpr int kMaxPeers = 8;
+struct Peers {
+  void* out[kMaxPeers];
+  int world, rank;
+};
+
+template <bool kF32Out, bool kGather = false>
 __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ ws, size_t off_cum, size_t off_lse,
                                                       size_t off_o, int batch, int num_heads,
-                                                      void* __restrict__ out, float* __restrict__ lse_out) {
+                                                      void* __restrict__ out, float* __restrict__ lse_out,
+                                                      const Peers peers = Peers{}) {
   const int lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (idx >= batch * num_heads) return;
@@ -66,9 +77,19 @@ __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ w
       __nv_bfloat162 v = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
       wv[i] = *reinterpret_cast<uint32_t*>(&v);
     }
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + orow);
-    dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    if constexpr (kGather) {
+      // row (b, rank * num_heads + h) of the [batch, world * num_heads, 512] output of every rank
+      const int64_t grow = ((int64_t)b * peers.world * num_heads + (int64_t)peers.rank * num_heads + h) * kDc + lane * 16;
+      for (int r = 0; r < peers.world; ++r) {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(peers.out[r]) + grow);
+        dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+      }
+    } else {
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + orow);
+      dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    }
   }
   if (lse_out && lane == 0) lse_out[idx] = lse;
 }
@@ -95,6 +116,34 @@ static mla_status launch_combine(const void* workspace, int batch, int num_heads
 }  // namespace snapmla
 
 using namespace snapmla;
+
+extern "C" mla_status mla_combine_gather(const void* workspace, int batch, int num_heads, int kv_lora_rank,
+                                         void* const* out_peers, int world, int rank, float* lse,
+                                         mla_stream_t stream) {
+  if (batch < 0 || num_heads <= 0) return MLA_ERR_SHAPE;
+  if (kv_lora_rank != kDc) return MLA_ERR_UNSUPPORTED;
+  if (num_heads > kMaxRows || world < 1 || world > kMaxPeers) return MLA_ERR_UNSUPPORTED;
+  if (rank < 0 || rank >= world) return MLA_ERR_SHAPE;
+  if (batch == 0) return MLA_OK;
+  if (!workspace) return MLA_ERR_WORKSPACE;
+  if (!out_peers) return MLA_ERR_NULL;
+  Peers peers = {};
+  peers.world = world;
+  peers.rank = rank;
+  for (int r = 0; r < world; ++r) {
+    if (!out_peers[r]) return MLA_ERR_NULL;
+    if (!aligned(out_peers[r], 16)) return MLA_ERR_ALIGN;
+    peers.out[r] = out_peers[r];
+  }
+  if (!aligned(workspace, 256)) return MLA_ERR_ALIGN;
+  const int sms = device_num_sms();
+  if (sms <= 0) return MLA_ERR_CUDA;
+  const WsLayout wl = ws_layout(batch, num_heads, sms);
+  const int n = batch * num_heads;
+  combine_kernel<false, true><<<(n + 3) / 4, 128, 0, (cudaStream_t)stream>>>(
+      static_cast<const char*>(workspace), wl.cum, wl.lse, wl.o, batch, num_heads, nullptr, lse, peers);
+  return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}
 
 extern "C" mla_status mla_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out,
                                   float* lse, mla_stream_t stream) {

@@ -6,7 +6,13 @@ DP  (batch partition): rank r owns requests [r*B/W, (r+1)*B/W) with its own
     pools and block table; no collective on the data path.
 TP  (head partition): rank r owns heads [r*H/W, (r+1)*H/W); MLA's latent is
     shared by all heads, so every rank holds (and appends) the full KV cache;
-    one all-gather of the BF16 output [B, H/W, 512] per step.
+    one all-gather of the BF16 output [B, H/W, 512] per step -- NCCL
+    (tp_gather_heads) or fused into the combine epilogue as peer stores
+    (mla_combine_gather over symmetric-memory buffers, NEXT-4(c)).
+DPxTP (hybrid, the paper's DP4/TP2-style deployments, P:456): world = D x T;
+    rank r = d * T + t owns requests dp_range(B, D, d) and heads
+    tp_range(H, T, t); the T ranks of a DP replica (consecutive ranks) form
+    the TP group that gathers heads.
 """
 import torch
 import torch.distributed as dist
@@ -37,3 +43,34 @@ def tp_gather_heads(out_local, group=None, gathered=None):
     dist.all_gather_into_tensor(gathered.view(-1), out_local.contiguous().view(-1), group=group)
     w, b, hl, d = gathered.shape
     return gathered.permute(1, 0, 2, 3).reshape(b, w * hl, d)
+
+
+def dptp_coords(world, tp, rank):
+    """(dp index, tp index) of `rank` in a world = (world // tp) x tp grid; TP groups are
+    consecutive ranks."""
+    if tp < 1 or world % tp:
+        raise ValueError(f"world={world} not divisible by tp={tp}")
+    return rank // tp, rank % tp
+
+
+def dptp_groups(world, tp):
+    """Create the TP subgroups {d*tp, ..., d*tp + tp - 1} (a collective: every rank calls it
+    with the same arguments) and return this rank's group."""
+    groups = [dist.new_group(list(range(d * tp, (d + 1) * tp))) for d in range(world // tp)]
+    return groups[dist.get_rank() // tp]
+
+
+def symmetric_gather_output(shape, group, device):
+    """A bf16 output buffer of `shape` in symmetric memory on every rank of `group`, and the
+    device pointers of all ranks' copies (rank order) for mla_combine_gather's peer stores."""
+    import torch.distributed._symmetric_memory as symm_mem
+    buf = symm_mem.empty(*shape, dtype=torch.bfloat16, device=device)
+    hdl = symm_mem.rendezvous(buf, group)
+    return buf, [int(p) for p in hdl.buffer_ptrs]
+
+
+def stream_barrier(group=None, device=None):
+    """Stream-ordered barrier (one-element all-reduce): peer stores issued before it on
+    every rank are visible to every rank after it."""
+    t = torch.zeros(1, dtype=torch.int32, device=device)
+    dist.all_reduce(t, group=group)

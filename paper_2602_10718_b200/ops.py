@@ -53,6 +53,8 @@ def lib():
     L.mla_combine.argtypes = [_P, _I, _I, _I, _P, _P, _P]
     L.mla_combine_f32.restype = _I
     L.mla_combine_f32.argtypes = [_P, _I, _I, _I, _P, _P, _P]
+    L.mla_combine_gather.restype = _I
+    L.mla_combine_gather.argtypes = [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p), _I, _I, _P, _P]
     L.mla_kv_append_bf16.restype = _I
     L.mla_kv_append_bf16.argtypes = [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _P, _P, _P]
     L.mla_decode_bf16.restype = _I
@@ -68,7 +70,7 @@ def lib():
 def exported_symbols():
     return ["mla_status_str", "mla_abi_version", "mla_kv_append_quant", "mla_decode_workspace_bytes",
             "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant",
-            "mla_kv_append_bf16", "mla_decode_bf16"]
+            "mla_kv_append_bf16", "mla_decode_bf16", "mla_combine_gather"]
 
 
 def _check(status, what):
@@ -136,6 +138,24 @@ def mla_combine(workspace, batch, num_heads, out, lse=None, stream=None):
     _check(lib().mla_combine(
         _dev(workspace, torch.uint8, "workspace"), batch, num_heads, D_C, _dev(out, torch.bfloat16, "out"),
         None if lse is None else _dev(lse, torch.float32, "lse"), _stream(stream)), "mla_combine")
+
+
+def mla_combine_gather(workspace, batch, num_heads, out_peers, rank, lse=None, stream=None):
+    """NEXT-4(c): combine + fused TP all-gather.  `out_peers`: one entry per rank -- a CUDA
+    bf16 tensor [batch, world * num_heads, 512] (local buffers on one GPU) or an int device
+    pointer of a peer-mapped buffer of that shape (e.g. symmetric-memory buffer_ptrs)."""
+    world = len(out_peers)
+    ptrs = (ctypes.c_void_p * world)()
+    for i, o in enumerate(out_peers):
+        if isinstance(o, torch.Tensor):
+            if o.shape != (batch, world * num_heads, D_C):
+                raise ValueError(f"out_peers[{i}]: expected [{batch}, {world * num_heads}, {D_C}], got {tuple(o.shape)}")
+            ptrs[i] = _dev(o, torch.bfloat16, f"out_peers[{i}]").value
+        else:
+            ptrs[i] = int(o)
+    _check(lib().mla_combine_gather(
+        _dev(workspace, torch.uint8, "workspace"), batch, num_heads, D_C, ptrs, world, rank,
+        None if lse is None else _dev(lse, torch.float32, "lse"), _stream(stream)), "mla_combine_gather")
 
 
 def mla_combine_f32(workspace, batch, num_heads, out, lse=None, stream=None):

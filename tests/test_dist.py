@@ -73,3 +73,49 @@ def test_tp_range_requires_divisible():
     assert D.tp_range(128, 8, 3) == (48, 64)
     with pytest.raises(ValueError):
         D.tp_range(10, 4, 0)
+
+
+# ---- DP x TP hybrid (NEXT-4(c)): world 4 = DP2 x TP2, gloo on CPU
+def _hybrid_worker(rank, world, tp, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, H, Dd = 6, 8, 512
+        full = torch.arange(B * H * Dd, dtype=torch.float32).view(B, H, Dd)
+        d, t = D.dptp_coords(world, tp, rank)
+        group = D.dptp_groups(world, tp)
+        b0, b1 = D.dp_range(B, world // tp, d)
+        h0, h1 = D.tp_range(H, tp, t)
+        got = D.tp_gather_heads(full[b0:b1, h0:h1].contiguous(), group=group)
+        ok_gather = bool(torch.equal(got, full[b0:b1]))
+        # every (request, head) computed by exactly one rank
+        own = torch.zeros(B, H, dtype=torch.int64)
+        own[b0:b1, h0:h1] = 1
+        dist.all_reduce(own)
+        D.stream_barrier(group=group)
+        q.put((rank, ok_gather, bool(torch.all(own == 1))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dptp_hybrid_gloo():
+    world, tp = 4, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hybrid_worker, args=(r, world, tp, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok_gather, ok_own in res:
+        assert ok_gather and ok_own, rank
+
+
+def test_dptp_coords():
+    assert [D.dptp_coords(8, 2, r) for r in range(4)] == [(0, 0), (0, 1), (1, 0), (1, 1)]
+    assert D.dptp_coords(8, 8, 5) == (0, 5)
+    with pytest.raises(ValueError):
+        D.dptp_coords(6, 4, 0)
