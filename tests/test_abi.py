@@ -77,6 +77,20 @@ def test_host_validation_without_gpu(L):
     assert L.mla_decode_fp8(fake, fake, fake, fake, fake, fake, 2, 16, 512, 64, 64, 4, 8, 0.1, None, 0,
                             None) == 5
     assert L.mla_combine(fake, 2, 16, 256, fake, None, None) == 3
+    # NEXT-2 BF16 baseline: same host checks
+    assert L.mla_kv_append_bf16(fake, fake, fake, fake, 4, 256, 64, 64, 1, 8, fake, fake, None) == 3
+    assert L.mla_kv_append_bf16(fake, None, fake, fake, 4, 512, 64, 64, 1, 8, fake, fake, None) == 1
+    assert L.mla_kv_append_bf16(fake, fake, fake, fake, 4, 512, 64, 64, 1, 8, P(4104), fake, None) == 4
+    assert L.mla_decode_bf16(fake, fake, fake, fake, fake, 2, 16, 1, 512, 64, 32, 4, 8, 0.1, fake, 1 << 20,
+                             None) == 3
+    assert L.mla_decode_bf16(fake, fake, fake, fake, fake, 2, 16, 1, 512, 64, 64, 4, 8, 0.1, None, 0, None) == 5
+    assert L.mla_decode_bf16(fake, None, fake, fake, fake, 2, 16, 1, 512, 64, 64, 4, 8, 0.1, fake, 1 << 30,
+                             None) == 1
+    # NEXT-4(c) fused gather: > 8 peers unsupported, rank outside the world, NULL peer
+    peers = (P * 9)(*([4096] * 9))
+    assert L.mla_combine_gather(fake, 2, 16, 512, peers, 9, 0, None, None) == 3
+    assert L.mla_combine_gather(fake, 2, 16, 512, peers, 2, 2, None, None) == 2
+    assert L.mla_combine_gather(fake, 2, 16, 512, (P * 2)(4096, None), 2, 0, None, None) == 1
 
 
 def test_workspace_size_formula(L):
