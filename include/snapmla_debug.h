@@ -12,9 +12,10 @@ extern "C" {
  * PV_R issue, softmax start, softmax done, O_L rescaled, O_R rescaled} of the
  * CTA's n-th key block.  NULL disables it (default). */
 void mla_debug_set_trace(unsigned long long* dev_buf);
-/* v != 0: decodes with 64 < rows <= 128 run on the experimental CTA-pair kernel
- * (cta_group::2 QK shared by the two head tiles of a key range)
- * instead of the default single-CTA kernel.  Process-global; default 0. */
+/* Decodes with 64 < rows <= 128 run on an experimental CTA-pair kernel instead of
+ * the default single-CTA kernel: v = 1 the pair kernel (cta_group::2 QK over two
+ * key blocks, per-CTA PV), v = 2 the 2-SM kernel (cta_group::2 QK
+ * and PV with token / dims halves per CTA; §7.8).  Process-global; default 0. */
 void mla_debug_set_pair(int v);
 /* Cap the number of CTA pairs the pair kernel launches (0 = as many as fit);
  * returns the cudaOccupancyMaxActiveClusters limit seen on the last pair launch

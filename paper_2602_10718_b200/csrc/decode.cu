@@ -1423,6 +1423,528 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
 }
 
+// ===================================================================== 2-SM kernel
+// 64 < rows <= 128 as a CTA pair that splits BOTH contractions the way the 2-SM datapath
+// wants (scripts/pair_probe.cu: CTA c holds D[r, n] at lane r for the N/2 columns of CTA 0's
+// B operand and at lane 64 + r for CTA 1's):
+//   QK  cta_group::2, M = 128 (64 rows per CTA), N = 64: CTA c supplies tokens [32c, 32c+32)
+//       of the block (K operand 16 KB + RoPE 4 KB); every CTA gets S for its rows with
+//       tokens 0-31 on lanes 0-63 and tokens 32-63 on lanes 64-127;
+//   PV  cta_group::2, M = 128, N = 256 twice: CTA c supplies V dims [256c, 256c+256) (16 KB);
+//       T_L holds dims [0,128) / [256,384) on lanes 0-63 / 64-127, T_R [128,256) / [384,512).
+// 36 KB per block per CTA (5 in flight); tensor time per block and SM ~half of the single-CTA
+// kernel's.  Softmax: thread = (row, token half) on SMSP (half, row / 32); the two halves of a
+// row exchange max / sum through SMEM (named barrier per SMSP pair).  Accumulators: thread =
+// (row, dims half of CTA), two warps per SMSP split the 128 columns, 128 fp32 of O each.
+// The leader (rank 0) issues all MMAs; the peer's P' is published to it by a 16-byte bulk
+// copy completing the leader's pp_full (the peer's PV warp forwards it).
+constexpr int k2Slots = 5;
+constexpr uint32_t k2Stage = 37888;                    // Kq 4 x 4 KB | RoPE 4 KB | V 2 x 8 KB | scales
+constexpr uint32_t k2OffRope = 16384, k2OffV = 20480, k2OffSc = 36864;
+constexpr uint32_t k2Tx = 36864;                       // TMA bytes per block per CTA (scales separate)
+constexpr uint32_t k2OffQr = 0, k2OffP = 8192, k2OffKv = 16384;
+constexpr uint32_t k2OffBar = k2OffKv + k2Slots * k2Stage;
+constexpr uint32_t k2Smem = k2OffBar + 8192 + 1024;
+static_assert(k2Smem <= 232448, "shared memory budget (2-SM kernel)");
+constexpr uint32_t kIdescQk8S = make_idesc(0, 0, 0, 0, 128, 64);
+constexpr uint32_t kIdescQk16S = make_idesc(1, 1, 0, 0, 128, 64);
+constexpr uint32_t kIdescPvS = make_idesc(0, 0, 0, 1, 128, 256);
+// TMEM: S slot ss at cols 32 ss; q codes (QK A operand, lanes 0-63) at cols 64-191; T half
+// slot t at cols 192 + 128 t.
+constexpr uint32_t k2TmemQ = 64, k2TmemT = 192;
+
+struct Bars2 {
+  alignas(16) uint8_t sink[kPSlots][16];   // landing bytes of the peer's P' signal (bulk-copy aligned)
+  uint64_t kv_full[k2Slots];    // leader: Kq + RoPE + V of both CTAs (cta_group::2 TMA)
+  uint64_t sc_full[k2Slots];    // local: sigma_K of the block
+  uint64_t kv_empty[k2Slots];   // PV_L + PV_R commits (multicast)
+  uint64_t s_full[kSSlots], s_empty[kSSlots];
+  uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
+  uint64_t t_full[2], t_free[2];
+  uint64_t q_full, q_free;
+  uint32_t tmem_base;
+  float crow[64];
+  float xm[2][2][64];           // [block parity][token half][row] partial max of t
+  float xl[2][2][64], xw[2][2][64];   // partial l and max of w
+  float stat[kPSlots][3][64];
+};
+static_assert(sizeof(Bars2) <= 8192, "barrier region (2-SM kernel)");
+#define B2(field) (bar0 + (uint32_t)offsetof(Bars2, field))
+
+#define SNAPMLA_QK8S(ta, bo, acc)                                                              \
+  "add.u32 t, %1, " #ta ";\n\tadd.s64 b, %2, " #bo ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [t], b, %3, " acc ";\n\t"
+#define SNAPMLA_QK16S(ao)                                                                      \
+  "add.s64 a, %4, " #ao ";\n\tadd.s64 b, %5, " #ao ";\n\t"                                     \
+  "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %6, pt;\n\t"
+// K operand boxes are 32 rows x 128 B (4 KB apart): K step kk at (kk / 4) * 4096 + (kk % 4) * 32
+__device__ __forceinline__ void qk_issue_2sm(uint32_t dS, uint32_t tQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
+                                             uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, t;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      SNAPMLA_QK8S(0, 0, "pf") SNAPMLA_QK8S(8, 2, "pt") SNAPMLA_QK8S(16, 4, "pt") SNAPMLA_QK8S(24, 6, "pt")
+      SNAPMLA_QK8S(32, 256, "pt") SNAPMLA_QK8S(40, 258, "pt") SNAPMLA_QK8S(48, 260, "pt") SNAPMLA_QK8S(56, 262, "pt")
+      SNAPMLA_QK8S(64, 512, "pt") SNAPMLA_QK8S(72, 514, "pt") SNAPMLA_QK8S(80, 516, "pt") SNAPMLA_QK8S(88, 518, "pt")
+      SNAPMLA_QK8S(96, 768, "pt") SNAPMLA_QK8S(104, 770, "pt") SNAPMLA_QK8S(112, 772, "pt") SNAPMLA_QK8S(120, 774, "pt")
+      SNAPMLA_QK16S(0) SNAPMLA_QK16S(2) SNAPMLA_QK16S(4) SNAPMLA_QK16S(6)
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %8;\n\t}"
+      ::"r"(dS), "r"(tQ), "l"(dK), "r"(kIdescQk8S), "l"(dQr), "l"(dKr), "r"(kIdescQk16S), "r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// One PV half (cta_group::2, N = 256 = 128 dims from each CTA): 2 x K = 32; commits multicast
+// to t_full, p_empty and kv_empty of both CTAs.
+__device__ __forceinline__ void pv_issue_2sm(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t, uint32_t bar_p,
+                                             uint32_t bar_kv) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%4], %7;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %7;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], %7;\n\t}"
+      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPvS), "r"(bar_t), "r"(bar_p), "r"(bar_kv), "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mla_decode_2sm_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv32,
+                          const __grid_constant__ CUtensorMap tm_rope32, const DecodeParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = sbase + k2OffBar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < k2Slots; ++i) {
+      mbar_init(B2(kv_full) + 8 * i, 1);
+      mbar_init(B2(sc_full) + 8 * i, 1);
+      mbar_init(B2(kv_empty) + 8 * i, 2);
+    }
+    for (int i = 0; i < kSSlots; ++i) {
+      mbar_init(B2(s_full) + 8 * i, 1);
+      mbar_init(B2(s_empty) + 8 * i, 8);       // 4 local + 4 peer softmax warps (leader's copy)
+    }
+    for (int i = 0; i < kPSlots; ++i) {
+      mbar_init(B2(p_full) + 8 * i, 4);        // local softmax warps (stats + P')
+      mbar_init(B2(pp_full) + 8 * i, 1);       // leader: the peer's P' (relaxed arrive + 16 B copy)
+      mbar_init(B2(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 local accumulator warps
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(B2(t_full) + 8 * i, 1);
+      mbar_init(B2(t_free) + 8 * i, 16);       // 8 local + 8 peer accumulator warps (leader's copy)
+    }
+    mbar_init(B2(q_full), 8);                  // the 4 prologue warps of both CTAs
+    mbar_init(B2(q_free), 1);
+    fence_barrier_init();
+  }
+  if (warp == kWarpTma && lane == 0) {
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_kv32);
+    tma_prefetch_desc(&tm_rope32);
+  }
+  if (warp == kWarpQk) tmem_alloc_pair(B2(tmem_base), 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = lds_u32(B2(tmem_base));
+
+  pdl_wait();
+  const int ht = (int)cta;
+  const int g = blockIdx.x / 2;
+  const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
+  const int lo = g * per;
+  const bool has_work = g < groups && lo < total;
+  const int hi = min(total, lo + per);
+  UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
+  Unit u;
+
+  if (warp >= kWarpTma && warp < kWarpSoftmax) {
+    regs_dec<kRegsIssue>();
+    if (warp == kWarpTma) {
+      // ============================ TMA producer (both CTAs) ============================
+      if (lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        const uint32_t kv_full_leader = mapa_shared(B2(kv_full), 0);
+        uint32_t n = 0;
+        while (it.next(u)) {
+          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          for (int j = u.k0; j < u.k1; ++j, ++n) {
+            const uint32_t st = n % k2Slots;
+            mbar_wait_backoff(B2(kv_empty) + 8 * st, ((n / k2Slots) & 1) ^ 1);
+            const int row = __ldg(bt + j) * kPage;
+            const uint32_t slot = sbase + k2OffKv + st * k2Stage;
+            const uint32_t sc = B2(sc_full) + 8 * st;
+            mbar_arrive_expect_tx(sc, 256);
+            bulk_load(slot + k2OffSc, p.kv_scale + (int64_t)row, 128, sc, pol);
+            bulk_load(slot + k2OffSc + 128, p.kv_scale + (int64_t)row + 32, 128, sc, pol);
+            if (leader) mbar_arrive_expect_tx(B2(kv_full) + 8 * st, 2 * k2Tx);
+            const uint32_t fb = kv_full_leader + 8 * st;
+            const int rq = row + 32 * (int)cta;   // this CTA's token half (QK operand)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tma_load_2d_cg2(slot + c * 4096, &tm_kv32, fb, c * 128, rq, pol);
+            tma_load_2d_cg2(slot + k2OffRope, &tm_rope32, fb, 0, rq, pol);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)           // this CTA's dims half of V (PV operand)
+              tma_load_2d_cg2(slot + k2OffV + i * kBoxBytes, &tm_kv, fb, (2 * (int)cta + i) * 128, row, pol);
+          }
+        }
+      }
+    } else if (warp == kWarpQk) {
+      // ================================ QK issuer (leader) ================================
+      if (leader) {
+        const uint64_t dQr = make_smem_desc(sbase + k2OffQr, 16, 1024, LAYOUT_SW128);
+        uint32_t n = 0, unit = 0;
+        while (it.next(u)) {
+          mbar_wait(B2(q_full), unit & 1, 2, unit);
+          for (int j = u.k0; j < u.k1; ++j, ++n) {
+            const uint32_t st = n % k2Slots, ss = n % kSSlots;
+            mbar_wait(B2(kv_full) + 8 * st, (n / k2Slots) & 1, 3, n);
+            mbar_wait(B2(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
+            tc_fence_after();
+            const uint32_t kv = sbase + k2OffKv + st * k2Stage;
+            qk_issue_2sm(tmem + 32 * ss, tmem + k2TmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
+                         make_smem_desc(kv + k2OffRope, 16, 1024, LAYOUT_SW128), B2(s_full) + 8 * ss);
+          }
+          mma_commit_pair_ws(B2(q_free));
+          ++unit;
+        }
+      }
+    } else if (leader) {
+      // ============================ PV_L / PV_R issuers (leader) ============================
+      const uint32_t half = warp - kWarpPv;
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t st = n % k2Slots, ps = n % kPSlots;
+          const uint32_t h = 2 * n + half, ts = h % 2;
+          mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
+          mbar_wait(B2(pp_full) + 8 * ps, (n / kPSlots) & 1, 14, n);
+          if (h >= 2) mbar_wait(B2(t_free) + 8 * ts, (h / 2 - 1) & 1, 6, n);
+          tc_fence_after();
+          const uint32_t pA = sbase + k2OffP + ps * 4096;
+          const uint32_t vb = sbase + k2OffKv + st * k2Stage + k2OffV + half * kBoxBytes;
+          pv_issue_2sm(tmem + k2TmemT + 128 * ts, make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
+                       make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), B2(t_full) + 8 * ts, B2(p_empty) + 8 * ps,
+                       B2(kv_empty) + 8 * st);
+        }
+      }
+    } else if (warp == kWarpPv) {
+      // ====================== peer: forward "P' written" to the leader ======================
+      const uint32_t pp_leader = mapa_shared(B2(pp_full), 0);
+      const uint32_t sink_leader = mapa_shared(B2(sink), 0);
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t ps = n % kPSlots;
+          mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 15, n);
+          if (lane == 0) mbar_signal_peer_tx(pp_leader + 8 * ps, sink_leader + 16 * ps, sbase + k2OffP + ps * 4096);
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= kWarpSoftmax) {
+    if constexpr (kRegsSoftmax > 128) regs_inc<kRegsSoftmax>();
+    else regs_dec<kRegsSoftmax>();
+    const int k = warp & 3;                  // SMSP: row group k & 1, token half k >> 1
+    const int hk = k >> 1;
+    const int r = 32 * (k & 1) + lane;       // row inside the head tile
+    const int head = ht * kHeadTile + r;
+    const bool row_ok = head < p.num_heads;
+    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
+    const uint32_t pair_bar = 2 + (k & 1);   // named barrier of the SMSP pair (k, k ^ 2)
+    const uint32_t s_empty_leader = mapa_shared(B2(s_empty), 0);
+    const uint32_t q_full_leader = mapa_shared(B2(q_full), 0);
+    uint32_t n = 0, unit = 0;
+    while (it.next(u)) {
+      // ---------------- Fused-Q-Quant prologue (a2).  The 2-SM QK reads its TMEM A operand
+      // per N half: rows for the CTA-0 token half from lanes 0-63, for the CTA-1 half from
+      // lanes 64-127 (measured: scripts/exp/dbg_2sm_s.py), so every warp writes the codes
+      // of its 32 rows into its own lane quarter; SMSPs 0-1 also write q_r' and c.
+      if (unit > 0) {
+        mbar_wait(B2(q_free), (unit - 1) & 1, 11, unit);
+        named_bar_sync(1, 128);
+      }
+      {
+        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
+        float amax = 0.f;
+        for (int c8 = 0; c8 < 64; c8 += 8) {
+          uint4 qv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + c8 + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(hv[e]);
+              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+            }
+          }
+        }
+        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
+        const float rsq = __frcp_rn(sq);
+        if (hk == 0) sts_f32(B2(crow) + 4 * r, sq * p.scale_log2);
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {     // 128 codes = 32 TMEM columns per store
+          uint32_t qa[32];
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            uint4 v2[2];
+            v2[0] = row_ok ? __ldg(qrow + 16 * cc + 2 * g8) : make_uint4(0, 0, 0, 0);
+            v2[1] = row_ok ? __ldg(qrow + 16 * cc + 2 * g8 + 1) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+              qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
+                                         div_by(f1.y, sq, rsq));
+            }
+          }
+          tmem_st_32x32b_x32(tmem + lane_base + k2TmemQ + 32 * cc, qa);
+        }
+        tmem_wait_st();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (hk) break;
+          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
+          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
+          uint32_t wd[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(a[e]);
+            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
+                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
+            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
+          }
+          sts_u4(sbase + k2OffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(B2(q_full));
+          else mbar_arrive_cluster(q_full_leader);
+        }
+      }
+      named_bar_sync(1, 128);
+      const float c_row = lds_f32(B2(crow) + 4 * r);
+      const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
+      float tt[32];
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        const uint32_t st = n % k2Slots, ss = n % kSSlots, ps = n % kPSlots, par = n & 1;
+        mbar_wait(B2(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
+        tc_fence_after();
+        tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(B2(s_empty) + 8 * ss);
+          else mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
+        }
+#ifdef SNAPMLA_DUMP_S
+        if (p.trace != nullptr && blockIdx.x < 2 && j == u.k0) {   // raw S of the first block (debug)
+          float* d = reinterpret_cast<float*>(p.trace);
+          for (int e = 0; e < 32; ++e) d[(ht * 64 + r) * 64 + 32 * hk + e] = tt[e];
+        }
+#endif
+        mbar_wait(B2(sc_full) + 8 * st, (n / k2Slots) & 1, 12, n);
+        const uint32_t sk = sbase + k2OffKv + st * k2Stage + k2OffSc + 128 * hk;
+        float4 skv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) skv[e] = lds_f4(sk + 16 * e);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 s4 = skv[e / 4];
+          const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4.x, s4.y));
+          const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4.z, s4.w));
+          tt[e] = a.x;
+          tt[e + 1] = a.y;
+          tt[e + 2] = b.x;
+          tt[e + 3] = b.y;
+        }
+        const int nvalid = L - (j * kBc + 32 * hk);
+        if (nvalid < 32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
+        }
+        float mx0 = fmaxf(fmaxf(tt[0], tt[1]), tt[2]), mx1 = fmaxf(fmaxf(tt[3], tt[4]), tt[5]);
+#pragma unroll
+        for (int e = 6; e < 30; e += 4) {
+          mx0 = fmaxf(fmaxf(mx0, tt[e]), tt[e + 1]);
+          mx1 = fmaxf(fmaxf(mx1, tt[e + 2]), tt[e + 3]);
+        }
+        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
+        // the other token half of this row lives on SMSP k ^ 2
+        sts_f32(B2(xm) + 4 * ((par * 2 + hk) * 64 + r), mx);
+        named_bar_sync(pair_bar, 64);
+        mx = fmaxf(mx, lds_f32(B2(xm) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r)));
+        const float mc = mx == -INFINITY ? 0.f : mx * c_row;
+        float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+        float mb0 = 0.f, mb1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 s4 = skv[e / 4];
+          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));
+          const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
+          const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));
+          const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
+          ls0 = __fadd2_rn(ls0, p0);
+          ls1 = __fadd2_rn(ls1, p1);
+          tt[e] = w0.x;
+          tt[e + 1] = w0.y;
+          tt[e + 2] = w1.x;
+          tt[e + 3] = w1.y;
+          mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
+          mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
+        }
+        float lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
+        float mb = fmaxf(mb0, mb1);
+        sts_f32(B2(xl) + 4 * ((par * 2 + hk) * 64 + r), lsum);
+        sts_f32(B2(xw) + 4 * ((par * 2 + hk) * 64 + r), mb);
+        named_bar_sync(pair_bar, 64);
+        lsum += lds_f32(B2(xl) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r));
+        mb = fmaxf(mb, lds_f32(B2(xw) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r)));
+        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
+        const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
+        const float2 inv2 = make_float2(inv, inv);
+        uint32_t pw[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
+          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
+          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+        }
+        mbar_wait(B2(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
+        if (hk == 0) {
+          const uint32_t sa = B2(stat) + ps * (3 * 64 * 4) + 4 * r;
+          sts_f32(sa, st_m);
+          sts_f32(sa + 256, st_sig);
+          sts_f32(sa + 512, lsum);
+        }
+        const uint32_t pdst = sbase + k2OffP + ps * 4096 + r * 16;
+        sts_u4(pdst + (2 * hk) * 1024, pw[0], pw[1], pw[2], pw[3]);
+        sts_u4(pdst + (2 * hk + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B2(p_full) + 8 * ps);
+      }
+      ++unit;
+    }
+  } else {
+    if constexpr (kRegsAcc > 128) regs_inc<kRegsAcc>();
+    else regs_dec<kRegsAcc>();
+    // ========= accumulators: thread = (row, CTA dims half), two warps per SMSP split columns =========
+    const int k = warp & 3, cg = warp >> 2;
+    const int r = 32 * (k & 1) + lane;
+    const int head = ht * kHeadTile + r;
+    const bool row_ok = head < p.num_heads;
+    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
+    const int dbase = (k >> 1) * 256 + 64 * cg;   // T_L column c -> dim dbase + c; T_R -> + 128
+    const uint32_t stat0 = B2(stat) + 4 * r;
+    const uint32_t t_free_leader = mapa_shared(B2(t_free), 0);
+    uint32_t n = 0;
+    while (it.next(u)) {
+      const uint32_t n0 = n;
+      float o[128];
+#pragma unroll
+      for (int e = 0; e < 128; ++e) o[e] = 0.f;
+      float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        const uint32_t ps = n % kPSlots;
+        mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        const uint32_t sa = stat0 + ps * (3 * 64 * 4);
+        const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B2(p_empty) + 8 * ps);
+        const float m_new = fmaxf(m_ref, mb);
+        const bool first = n == n0;
+        const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
+        float gamma = 0.f;
+        if (first) {
+          m_O = mb;
+          sig_O = sb;
+          l_run = lb;
+          m_ref = mb;
+        } else if (!skip) {
+          gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);
+          l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
+          m_ref = m_new;
+          m_O = mb;
+          sig_O = sb;
+        }
+        const float2 g2 = make_float2(gamma, gamma);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t h = 2 * n + hf, ts = h % 2;
+          mbar_wait(B2(t_full) + 8 * ts, (h / 2) & 1, 10, n);
+          tc_fence_after();
+          const uint32_t taddr = tmem + lane_base + k2TmemT + 128 * ts + 64 * cg;
+          uint32_t tv[2][16];
+          tmem_ld_32x32b_x16(taddr, tv[0]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tmem_wait_ld();
+            if (c < 3) tmem_ld_32x32b_x16(taddr + 16 * (c + 1), tv[(c + 1) & 1]);
+            else {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if (leader) mbar_arrive(B2(t_free) + 8 * ts);
+                else mbar_arrive_cluster_relaxed(t_free_leader + 8 * ts);
+              }
+            }
+            const uint32_t* cur = tv[c & 1];
+            if (!skip) {
+#pragma unroll
+              for (int e = 0; e < 16; e += 2) {
+                const int oi = 64 * hf + 16 * c + e;
+                const float2 a = __ffma2_rn(make_float2(o[oi], o[oi + 1]), g2,
+                                            make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
+                o[oi] = a.x;
+                o[oi + 1] = a.y;
+              }
+            }
+          }
+        }
+      }
+      const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;
+      const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
+      if (row_ok) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float* dst = p.o_part + prow * kDc + dbase + 128 * hf;
+#pragma unroll
+          for (int e = 0; e < 64; e += 4)
+            *reinterpret_cast<float4*>(dst + e) = make_float4(o[64 * hf + e] * f, o[64 * hf + e + 1] * f,
+                                                              o[64 * hf + e + 2] * f, o[64 * hf + e + 3] * f);
+        }
+        if (k < 2 && cg == 0)
+          p.lse_part[prow] = l_run > 0.f ? (m_ref + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kWarpQk) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1455,7 +1977,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 }
 
 static unsigned long long* g_trace = nullptr;
-static bool g_pair = false;   // experimental CTA-pair kernel for 64 < rows <= 128
+static int g_pair = 0;   // experimental kernels for 64 < rows <= 128: 1 = CTA pair (§7.6), 2 = 2-SM (§7.8)
 static int g_pair_groups = 0, g_pair_max_clusters = -1;   // debug: force the single-CTA kernel for 64 < rows <= 128
 
 int device_num_sms() {
@@ -1473,7 +1995,7 @@ using namespace snapmla;
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
 // Experimental: 1 = run 64 < rows <= 128 on the CTA-pair kernel instead of the default single-CTA
 // kernel (two CTAs per key range, each with its own M = 64 QK).
-extern "C" void mla_debug_set_pair(int v) { g_pair = v != 0; }
+extern "C" void mla_debug_set_pair(int v) { g_pair = v; }
 // Debug only: cap the number of CTA pairs of the pair kernel (0 = all that fit); returns the
 // occupancy limit cudaOccupancyMaxActiveClusters reported on the last pair launch (-1: none yet).
 extern "C" int mla_debug_set_pair_groups(int v) {
@@ -1510,8 +2032,25 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   if (workspace_bytes < wl.total) return MLA_ERR_WORKSPACE;
   const int n_ht = (num_heads + kHeadTile - 1) / kHeadTile;
-  const bool pair = !bf16 && n_ht == 2 && g_pair;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
+  const bool pair = !bf16 && n_ht == 2 && g_pair == 1;
+  const bool two_sm = !bf16 && n_ht == 2 && g_pair == 2;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
   int groups = sms / n_ht;
+  if (two_sm) {
+    static int max_clusters2 = -1;
+    if (max_clusters2 < 0) {
+      if (cudaFuncSetAttribute(mla_decode_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem) !=
+          cudaSuccess)
+        return MLA_ERR_CUDA;
+      cudaLaunchConfig_t oc = {};
+      oc.gridDim = dim3(2 * groups);
+      oc.blockDim = dim3(kThreads);
+      oc.dynamicSmemBytes = k2Smem;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, mla_decode_2sm_kernel, &oc) != cudaSuccess) return MLA_ERR_CUDA;
+      max_clusters2 = nc;
+    }
+    if (max_clusters2 > 0 && max_clusters2 < groups) groups = max_clusters2;
+  }
   if (pair) {
     static int max_clusters = -1;
     if (max_clusters < 0) {
@@ -1531,13 +2070,16 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
     if (g_pair_groups > 0 && g_pair_groups < groups) groups = g_pair_groups;
   }
 
-  CUtensorMap tm_kv, tm_rope;
+  CUtensorMap tm_kv, tm_rope, tm_kv32, tm_rope32;
   const uint64_t rows = (uint64_t)num_pages * kPage;
   if (num_pages == 0) return MLA_ERR_SHAPE;
   if (bf16 ? !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_fp8, kDc, rows, kDc * 2, 64, 64)
            : !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 64))
     return MLA_ERR_CUDA;
   if (!encode_2d(&tm_rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_rope, kDr, rows, kDr * 2, 64, 64))
+    return MLA_ERR_CUDA;
+  if (two_sm && (!encode_2d(&tm_kv32, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 32) ||
+                 !encode_2d(&tm_rope32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_rope, kDr, rows, kDr * 2, 64, 32)))
     return MLA_ERR_CUDA;
 
   char* ws = static_cast<char*>(workspace);
@@ -1548,8 +2090,8 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   plan_kernel<<<1, 1024, 0, st>>>(seq_lens, batch, num_heads, groups, hdr, cum, first);
   if (cudaGetLastError() != cudaSuccess) return MLA_ERR_CUDA;
 
-  const uint32_t smem = pair ? kPSmemBytes : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
-  if (!pair && cudaFuncSetAttribute(bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>,
+  const uint32_t smem = two_sm ? k2Smem : pair ? kPSmemBytes : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
+  if (!pair && !two_sm && cudaFuncSetAttribute(bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return MLA_ERR_CUDA;
   DecodeParams prm;
@@ -1585,7 +2127,10 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (pair) {
+  if (two_sm) {
+    if (cudaLaunchKernelEx(&cfg, mla_decode_2sm_kernel, tm_kv, tm_kv32, tm_rope32, prm) != cudaSuccess)
+      return MLA_ERR_CUDA;
+  } else if (pair) {
     if (cudaLaunchKernelEx(&cfg, mla_decode_pair_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
   } else if (cudaLaunchKernelEx(&cfg, bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>, tm_kv, tm_rope,
                                 prm) != cudaSuccess) {

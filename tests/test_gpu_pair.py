@@ -1,5 +1,5 @@
-"""Experimental CTA-pair kernel (include/snapmla_debug.h mla_debug_set_pair):
-64 < rows <= 128 with the two head tiles of a key range as a cta_group::2 pair.  Same O7
+"""Experimental CTA-pair kernels (include/snapmla_debug.h mla_debug_set_pair, DESIGN.md §7.6,
+§7.8): 64 < rows <= 128 with the two head tiles of a key range as a cta_group::2 pair.  Same O7
 gate as test_gpu_decode.py; the pair kernel must also agree bit for bit with itself
 across runs.  The switch is process-global, so every test restores the default."""
 import numpy as np
@@ -13,11 +13,12 @@ from test_gpu_mtp import _check_mtp
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def pair_kernel():
+@pytest.fixture(params=[1, 2], ids=["pair", "2sm"])
+def pair_kernel(request):
+    """1: CTA-pair kernel, 2: 2-SM kernel (§7.8)."""
     L = ops.lib()
-    L.mla_debug_set_pair(1)
-    yield
+    L.mla_debug_set_pair(request.param)
+    yield request.param
     L.mla_debug_set_pair(0)
 
 
