@@ -1439,6 +1439,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // The leader (rank 0) issues all MMAs; the peer's P' is published to it by a 16-byte bulk
 // copy completing the leader's pp_full (the peer's PV warp forwards it).
 constexpr int k2Slots = 5;
+#ifndef SNAPMLA_2SM_SPF
+#define SNAPMLA_2SM_SPF 0
+#endif
+#ifndef SNAPMLA_2SM_BULK
+#define SNAPMLA_2SM_BULK 0
+#endif
+constexpr bool k2SPrefetch = SNAPMLA_2SM_SPF, k2BulkSignal = SNAPMLA_2SM_BULK;
 constexpr uint32_t k2Stage = 37888;                    // Kq 4 x 4 KB | RoPE 4 KB | V 2 x 8 KB | scales
 constexpr uint32_t k2OffRope = 16384, k2OffV = 20480, k2OffSc = 36864;
 constexpr uint32_t k2Tx = 36864;                       // TMA bytes per block per CTA (scales separate)
@@ -1534,7 +1541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kPSlots; ++i) {
       mbar_init(B2(p_full) + 8 * i, 4);        // local softmax warps (stats + P')
-      mbar_init(B2(pp_full) + 8 * i, 1);       // leader: the peer's P' (relaxed arrive + 16 B copy)
+      mbar_init(B2(pp_full) + 8 * i, 1);       // leader: the peer's P' (its forwarding warp)
       mbar_init(B2(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 local accumulator warps
     }
     for (int i = 0; i < 2; ++i) {
@@ -1580,6 +1587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int j = u.k0; j < u.k1; ++j, ++n) {
             const uint32_t st = n % k2Slots;
             mbar_wait_backoff(B2(kv_empty) + 8 * st, ((n / k2Slots) & 1) ^ 1);
+            TRACE(TR_TMA, n);
             const int row = __ldg(bt + j) * kPage;
             const uint32_t slot = sbase + k2OffKv + st * k2Stage;
             const uint32_t sc = B2(sc_full) + 8 * st;
@@ -1608,8 +1616,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int j = u.k0; j < u.k1; ++j, ++n) {
             const uint32_t st = n % k2Slots, ss = n % kSSlots;
             mbar_wait(B2(kv_full) + 8 * st, (n / k2Slots) & 1, 3, n);
+            if (lane == 0) TRACE(TR_S2, n);
             mbar_wait(B2(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
             tc_fence_after();
+            if (lane == 0) TRACE(TR_QK, n);
             const uint32_t kv = sbase + k2OffKv + st * k2Stage;
             qk_issue_2sm(tmem + 32 * ss, tmem + k2TmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
                          make_smem_desc(kv + k2OffRope, 16, 1024, LAYOUT_SW128), B2(s_full) + 8 * ss);
@@ -1628,8 +1638,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t h = 2 * n + half, ts = h % 2;
           mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
           mbar_wait(B2(pp_full) + 8 * ps, (n / kPSlots) & 1, 14, n);
+          if (lane == 0 && half == 0) TRACE(TR_S5, n);
           if (h >= 2) mbar_wait(B2(t_free) + 8 * ts, (h / 2 - 1) & 1, 6, n);
           tc_fence_after();
+          if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
           const uint32_t pA = sbase + k2OffP + ps * 4096;
           const uint32_t vb = sbase + k2OffKv + st * k2Stage + k2OffV + half * kBoxBytes;
           pv_issue_2sm(tmem + k2TmemT + 128 * ts, make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
@@ -1638,15 +1650,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     } else if (warp == kWarpPv) {
-      // ====================== peer: forward "P' written" to the leader ======================
+      // ============ peer: forward "P' written" to the leader's PV issue (relaxed arrive) ============
+      // A release arrive on the remote barrier from the softmax warps themselves stalls them
+      // (~1-2K cycles, measured); this warp observes the local p_full (acquire: the softmax
+      // warps' SMEM writes and proxy fences precede it) and signals the leader.
       const uint32_t pp_leader = mapa_shared(B2(pp_full), 0);
-      const uint32_t sink_leader = mapa_shared(B2(sink), 0);
       uint32_t n = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t ps = n % kPSlots;
           mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 15, n);
-          if (lane == 0) mbar_signal_peer_tx(pp_leader + 8 * ps, sink_leader + 16 * ps, sbase + k2OffP + ps * 4096);
+          if (lane == 0) {
+            if constexpr (k2BulkSignal)
+              mbar_signal_peer_tx(pp_leader + 8 * ps, mapa_shared(B2(sink), 0) + 16 * ps, sbase + k2OffP + ps * 4096);
+            else
+              mbar_arrive_cluster_relaxed(pp_leader + 8 * ps);
+          }
           __syncwarp();
         }
       }
@@ -1738,12 +1757,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       const float c_row = lds_f32(B2(crow) + 4 * r);
       const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
+      // One exchange per block between the two token halves of a row: each half exponentiates
+      // against its OWN max m_h; then (m_h, l_h, max_h w) are exchanged and half h rescales by
+      // f_h = 2^{(m_h - m) c}: l = sum_h f_h l_h, M_b = max_h f_h max_h(w), P' = E4M3(w f_h 448 / M_b)
+      // (P' depends only on w / max_block(w)).  S(n+1) is loaded from TMEM before
+      // block n's P' / stats stores.
       float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % k2Slots, ss = n % kSSlots, ps = n % kPSlots, par = n & 1;
-        mbar_wait(B2(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
-        tc_fence_after();
-        tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        if (j == u.k0 || !k2SPrefetch) {
+          mbar_wait(B2(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
+          tc_fence_after();
+          tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -1751,13 +1778,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_arrive(B2(s_empty) + 8 * ss);
           else mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
         }
-#ifdef SNAPMLA_DUMP_S
-        if (p.trace != nullptr && blockIdx.x < 2 && j == u.k0) {   // raw S of the first block (debug)
-          float* d = reinterpret_cast<float*>(p.trace);
-          for (int e = 0; e < 32; ++e) d[(ht * 64 + r) * 64 + 32 * hk + e] = tt[e];
-        }
-#endif
         mbar_wait(B2(sc_full) + 8 * st, (n / k2Slots) & 1, 12, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
         const uint32_t sk = sbase + k2OffKv + st * k2Stage + k2OffSc + 128 * hk;
         float4 skv[8];
 #pragma unroll
@@ -1783,19 +1805,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mx0 = fmaxf(fmaxf(mx0, tt[e]), tt[e + 1]);
           mx1 = fmaxf(fmaxf(mx1, tt[e + 2]), tt[e + 3]);
         }
-        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));
-        // the other token half of this row lives on SMSP k ^ 2
-        sts_f32(B2(xm) + 4 * ((par * 2 + hk) * 64 + r), mx);
-        named_bar_sync(pair_bar, 64);
-        mx = fmaxf(mx, lds_f32(B2(xm) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r)));
-        const float mc = mx == -INFINITY ? 0.f : mx * c_row;
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));   // this half's max of t
+        const float mch = mx == -INFINITY ? 0.f : mx * c_row;
         float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
         float mb0 = 0.f, mb1 = 0.f;
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
           const float4 s4 = skv[e / 4];
-          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
-          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mch, -mch));
+          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mch, -mch));
           const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));
           const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
           const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));
@@ -1809,15 +1827,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
           mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
         }
-        float lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
-        float mb = fmaxf(mb0, mb1);
-        sts_f32(B2(xl) + 4 * ((par * 2 + hk) * 64 + r), lsum);
-        sts_f32(B2(xw) + 4 * ((par * 2 + hk) * 64 + r), mb);
+        const float lsh = (ls0.x + ls0.y) + (ls1.x + ls1.y);
+        const float mbh = fmaxf(mb0, mb1);
+        const uint32_t xo = 4 * ((par * 2 + hk) * 64 + r), xp = 4 * ((par * 2 + (hk ^ 1)) * 64 + r);
+        sts_f32(B2(xm) + xo, mx);
+        sts_f32(B2(xl) + xo, lsh);
+        sts_f32(B2(xw) + xo, mbh);
         named_bar_sync(pair_bar, 64);
-        lsum += lds_f32(B2(xl) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r));
-        mb = fmaxf(mb, lds_f32(B2(xw) + 4 * ((par * 2 + (hk ^ 1)) * 64 + r)));
+        const float mxo = lds_f32(B2(xm) + xp), lso = lds_f32(B2(xl) + xp), mbo = lds_f32(B2(xw) + xp);
+        const float mtot = fmaxf(mx, mxo);
+        const float mc = mtot == -INFINITY ? 0.f : mtot * c_row;
+        const float fme = mx == -INFINITY ? 0.f : ex2_approx(mch - mc);          // f_h of this half
+        const float fot = mxo == -INFINITY ? 0.f : ex2_approx(mxo * c_row - mc); // f_h of the other half
+        const float lsum = lsh * fme + lso * fot;
+        const float mb = fmaxf(mbh * fme, mbo * fot);
         const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
-        const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
+        const float inv = mb > 0.f ? __fdividef(448.0f, mb) * fme : 0.f;
         const float2 inv2 = make_float2(inv, inv);
         uint32_t pw[8];
 #pragma unroll
@@ -1826,7 +1851,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
           pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
         }
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
+        if (k2SPrefetch && j + 1 < u.k1) {   // prefetch S(n+1)
+          const uint32_t ss1 = (n + 1) % kSSlots;
+          mbar_wait(B2(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
+          tc_fence_after();
+          tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
+        }
         mbar_wait(B2(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
         if (hk == 0) {
           const uint32_t sa = B2(stat) + ps * (3 * 64 * 4) + 4 * r;
           sts_f32(sa, st_m);
@@ -1838,7 +1871,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sts_u4(pdst + (2 * hk + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(p_full) + 8 * ps);
+        if (lane == 0) mbar_arrive(B2(p_full) + 8 * ps);   // local: P' + stats written
+        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
       ++unit;
     }
@@ -1864,6 +1898,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t ps = n % kPSlots;
         mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        if (threadIdx.x == 0) TRACE(TR_C0, n);
         const uint32_t sa = stat0 + ps * (3 * 64 * 4);
         const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
         __syncwarp();
@@ -1917,6 +1952,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
+          if (threadIdx.x == 0) TRACE(hf == 0 ? TR_C_L : TR_C_R, n);
         }
       }
       const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;

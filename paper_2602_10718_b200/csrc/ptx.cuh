@@ -455,6 +455,13 @@ DEVI void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// arrive (release, CTA scope -- the default of mbarrier.arrive) on a barrier given by its
+// shared::cluster address, e.g. the pair leader's: publishes this CTA's prior SMEM writes
+// (after fence.proxy.async) to the leader's tensor-core reads, as CUTLASS's 2x1SM
+// umma_arrive does; far cheaper than a release at cluster scope
+DEVI void mbar_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
 // relaxed remote arrive.expect_tx + a 16-byte bulk copy completing it: publishes this CTA's
 // prior async-proxy-visible SMEM writes to the peer's waiter without a release fence
 DEVI void mbar_signal_peer_tx(uint32_t peer_bar, uint32_t peer_dst, uint32_t src) {
