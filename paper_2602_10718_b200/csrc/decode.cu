@@ -1537,7 +1537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(B2(s_full) + 8 * i, 1);
-      mbar_init(B2(s_empty) + 8 * i, 8);       // 4 local + 4 peer softmax warps (leader's copy)
+      mbar_init(B2(s_empty) + 8 * i, leader ? 4 + 1 : 4);   // leader: 4 local warps + the peer's forward; peer: local
     }
     for (int i = 0; i < kPSlots; ++i) {
       mbar_init(B2(p_full) + 8 * i, 4);        // local softmax warps (stats + P')
@@ -1546,7 +1546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(B2(t_full) + 8 * i, 1);
-      mbar_init(B2(t_free) + 8 * i, 16);       // 8 local + 8 peer accumulator warps (leader's copy)
+      mbar_init(B2(t_free) + 8 * i, leader ? 8 + 1 : 8);   // leader: 8 local warps + the peer's forward; peer: local
     }
     mbar_init(B2(q_full), 8);                  // the 4 prologue warps of both CTAs
     mbar_init(B2(q_free), 1);
@@ -1606,9 +1606,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (warp == kWarpQk) {
+    } else if (warp == kWarpQk && leader) {
       // ================================ QK issuer (leader) ================================
-      if (leader) {
+      {
         const uint64_t dQr = make_smem_desc(sbase + k2OffQr, 16, 1024, LAYOUT_SW128);
         uint32_t n = 0, unit = 0;
         while (it.next(u)) {
@@ -1647,6 +1647,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           pv_issue_2sm(tmem + k2TmemT + 128 * ts, make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
                        make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), B2(t_full) + 8 * ts, B2(p_empty) + 8 * ps,
                        B2(kv_empty) + 8 * st);
+        }
+      }
+    } else if (warp == kWarpQk) {
+      // ======== peer: forward "S slot read" (its 4 softmax warps, local barrier) to the leader ========
+      // (remote arrives issued by the compute warps themselves stall them; measured)
+      const uint32_t s_empty_leader = mapa_shared(B2(s_empty), 0);
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+          const uint32_t ss = n % kSSlots;
+          mbar_wait(B2(s_empty) + 8 * ss, (n / kSSlots) & 1, 16, n);
+          if (lane == 0) mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
+          __syncwarp();
+        }
+      }
+    } else if (warp == kWarpPv + 1) {
+      // ======== peer: forward "T half read" (its 8 accumulator warps, local barrier) to the leader ========
+      const uint32_t t_free_leader = mapa_shared(B2(t_free), 0);
+      uint32_t n = 0;
+      while (it.next(u)) {
+        for (int j = u.k0; j < u.k1; ++j, ++n) {
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait(B2(t_free) + 8 * hf, n & 1, 17, n);
+            if (lane == 0) mbar_arrive_cluster_relaxed(t_free_leader + 8 * hf);
+            __syncwarp();
+          }
         }
       }
     } else if (warp == kWarpPv) {
@@ -1774,10 +1801,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(B2(s_empty) + 8 * ss);
-          else mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
-        }
+        if (lane == 0) mbar_arrive(B2(s_empty) + 8 * ss);   // peer: forwarded by its warp 9
         mbar_wait(B2(sc_full) + 8 * st, (n / k2Slots) & 1, 12, n);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
         const uint32_t sk = sbase + k2OffKv + st * k2Stage + k2OffSc + 128 * hk;
@@ -1935,10 +1959,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             else {
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) {
-                if (leader) mbar_arrive(B2(t_free) + 8 * ts);
-                else mbar_arrive_cluster_relaxed(t_free_leader + 8 * ts);
-              }
+              if (lane == 0) mbar_arrive(B2(t_free) + 8 * ts);   // peer: forwarded by its warp 11
             }
             const uint32_t* cur = tv[c & 1];
             if (!skip) {
