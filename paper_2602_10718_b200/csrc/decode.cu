@@ -1443,7 +1443,7 @@ constexpr int k2Slots = 5;
 #define SNAPMLA_2SM_SPF 0
 #endif
 #ifndef SNAPMLA_2SM_BULK
-#define SNAPMLA_2SM_BULK 0
+#define SNAPMLA_2SM_BULK 1
 #endif
 constexpr bool k2SPrefetch = SNAPMLA_2SM_SPF, k2BulkSignal = SNAPMLA_2SM_BULK;
 constexpr uint32_t k2Stage = 37888;                    // Kq 4 x 4 KB | RoPE 4 KB | V 2 x 8 KB | scales
@@ -2034,7 +2034,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 }
 
 static unsigned long long* g_trace = nullptr;
-static int g_pair = 0;   // experimental kernels for 64 < rows <= 128: 1 = CTA pair (§7.6), 2 = 2-SM (§7.8)
+static int g_pair = 2;   // kernel for 64 < rows <= 128: 2 = 2-SM (default, §7.8), 1 = CTA pair (§7.6), 0 = single-CTA
 static int g_pair_groups = 0, g_pair_max_clusters = -1;   // debug: force the single-CTA kernel for 64 < rows <= 128
 
 int device_num_sms() {
@@ -2050,8 +2050,8 @@ using namespace snapmla;
 
 // Debug only (include/snapmla_debug.h): subsequent decodes record a CTA-0 event timeline.
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
-// Experimental: 1 = run 64 < rows <= 128 on the CTA-pair kernel instead of the default single-CTA
-// kernel (two CTAs per key range, each with its own M = 64 QK).
+// Kernel for 64 < rows <= 128: 2 = 2-SM kernel (default), 1 = CTA-pair kernel (experimental),
+// 0 = the single-CTA kernel (two CTAs per key range, each with its own M = 64 QK and PV).
 extern "C" void mla_debug_set_pair(int v) { g_pair = v; }
 // Debug only: cap the number of CTA pairs of the pair kernel (0 = all that fit); returns the
 // occupancy limit cudaOccupancyMaxActiveClusters reported on the last pair launch (-1: none yet).

@@ -7,6 +7,6 @@ python bench.py --impl reference > gpurun_out/${TAG}_bench_reference_dsr1.json 2
 for w in longcat dsr1_tp8; do python bench.py --workload $w --no-cpu-baseline > gpurun_out/${TAG}_bench_$w.json 2>/dev/null; done
 for w in dsr1 longcat dsr1_tp8; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_$w.csv python bench.py --workload $w --no-cpu-baseline --steps 2 --warmup 1 > /dev/null 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mla_decode_kernel -s 3 -c 1 -o gpurun_out/${TAG}_decode_$w python bench.py --workload $w --no-cpu-baseline --steps 2 --warmup 3 > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:mla_decode_ -s 3 -c 1 -o gpurun_out/${TAG}_decode_$w python bench.py --workload $w --no-cpu-baseline --steps 2 --warmup 3 > /dev/null 2>&1
 done
 ls -la gpurun_out | tail -20

@@ -67,7 +67,7 @@ def launch_shares(path):
     seq.sort()
     # the timed steps are the tail: append, plan, decode, combine repeated; keep from the first decode on
     names = [s[1] for s in seq]
-    first_dec = next(i for i, n in enumerate(names) if "mla_decode_kernel" in n)
+    first_dec = next(i for i, n in enumerate(names) if "mla_decode_" in n)
     # include the append/plan right before the first decode
     tail = seq[max(0, first_dec - 2):]
     agg = defaultdict(float)
@@ -103,7 +103,7 @@ def main():
             "grid": m["launch__grid_size"][0],
             "block": m["launch__block_size"][0],
         }
-        lines = [f"# ncu summary {tag} / {w}: mla_decode_kernel, one launch (--set full, --clock-control none)", ""]
+        lines = [f"# ncu summary {tag} / {w}: decode kernel (mla_decode_*), one launch (--set full, --clock-control none)", ""]
         for k, (v, u) in m.items():
             lines.append(f"{k:70s} {v} {u}")
         lp = os.path.join(OUT, f"{tag}_launches_{w}.csv")
@@ -112,7 +112,7 @@ def main():
             lines += ["", "# launch list (gpu__time_duration, serialized cold-cache; timed-step tail): kernel, total s, share"]
             for k, (v, f) in shares.items():
                 lines.append(f"{k[:80]:80s} {v:.6e} {100 * f:5.1f}%")
-            entry["decode_share_of_step_ncu"] = next((f for k, (v, f) in shares.items() if "mla_decode_kernel" in k), None)
+            entry["decode_share_of_step_ncu"] = next((f for k, (v, f) in shares.items() if "mla_decode_" in k), None)
         summary[w + ("_bf16" if "bf16" in tag else "")] = entry   # the BF16 baseline keeps its own key
         open(os.path.join(PROF, f"{tag}_ncu_{w}.txt"), "w").write("\n".join(lines) + "\n")
         print(w, json.dumps(entry))
