@@ -12,11 +12,11 @@ extern "C" {
  * PV_R issue, softmax start, softmax done, O_L rescaled, O_R rescaled} of the
  * CTA's n-th key block.  NULL disables it (default). */
 void mla_debug_set_trace(unsigned long long* dev_buf);
-/* Kernel for decodes with 64 < rows <= 128 (e.g. 128 heads): v = 2 the 2-SM
- * kernel (cta_group::2 QK and PV with token / dims halves per CTA of a cluster
- * pair; the default), v = 1 the CTA-pair kernel (cta_group::2 QK
- * over two key blocks, per-CTA PV; §7.6; experimental), v = 0 the single-CTA
- * kernel (two independent M = 64 CTAs per key range; §7.3).  Process-global. */
+/* Kernel for decodes with 64 < rows <= 128 (e.g. 128 heads): v = 0 the single-CTA
+ * kernel (two independent M = 64 CTAs per key range; the default),
+ * v = 2 the 2-SM kernel (cta_group::2 QK and PV with token / dims halves per CTA of
+ * a cluster pair; §7.8), v = 1 the CTA-pair kernel (cta_group::2 QK over two key
+ * blocks, per-CTA PV; §7.6).  v = 1, 2 are experimental.  Process-global. */
 void mla_debug_set_pair(int v);
 /* Cap the number of CTA pairs the pair kernel launches (0 = as many as fit);
  * returns the cudaOccupancyMaxActiveClusters limit seen on the last pair launch

@@ -2034,7 +2034,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 }
 
 static unsigned long long* g_trace = nullptr;
-static int g_pair = 2;   // kernel for 64 < rows <= 128: 2 = 2-SM (default, §7.8), 1 = CTA pair (§7.6), 0 = single-CTA
+static int g_pair = 0;   // kernel for 64 < rows <= 128: 0 = single-CTA (default), 2 = 2-SM (§7.8), 1 = CTA pair (§7.6)
 static int g_pair_groups = 0, g_pair_max_clusters = -1;   // debug: force the single-CTA kernel for 64 < rows <= 128
 
 int device_num_sms() {
@@ -2050,8 +2050,8 @@ using namespace snapmla;
 
 // Debug only (include/snapmla_debug.h): subsequent decodes record a CTA-0 event timeline.
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
-// Kernel for 64 < rows <= 128: 2 = 2-SM kernel (default), 1 = CTA-pair kernel (experimental),
-// 0 = the single-CTA kernel (two CTAs per key range, each with its own M = 64 QK and PV).
+// Kernel for 64 < rows <= 128: 0 = the single-CTA kernel (default; two CTAs per key range, each
+// with its own M = 64 QK and PV), 2 = 2-SM kernel, 1 = CTA-pair kernel (both experimental).
 extern "C" void mla_debug_set_pair(int v) { g_pair = v; }
 // Debug only: cap the number of CTA pairs of the pair kernel (0 = all that fit); returns the
 // occupancy limit cudaOccupancyMaxActiveClusters reported on the last pair launch (-1: none yet).
