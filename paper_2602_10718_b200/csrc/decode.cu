@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % V::kSlots, ss = n % kSSlots, ps = n % kPSlots;
-        if (j == u.k0) {
+        if (j == u.k0 || kBf) {
           mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
           tc_fence_after();
           tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
@@ -693,7 +693,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
-        if (j + 1 < u.k1) {   // prefetch S(n+1)
+        // prefetch S(n+1) (FP8 only: with the BF16 variant's 2-slot ring it ties P'(n) to the TMA
+        // of block n+1 and serialises the pipeline, measured 4x slower per block)
+        if (!kBf && j + 1 < u.k1) {
           const uint32_t ss1 = (n + 1) % kSSlots;
           mbar_wait(BAR(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
           tc_fence_after();
