@@ -285,6 +285,9 @@ __device__ __forceinline__ uint32_t t_slot_addr(uint32_t tmem, uint32_t s) {
 // unquantized cache / Q / P).  BF16: 8 content boxes + RoPE = 72 KB per block (two slots fit),
 // q content (1 KB per row) in TMEM columns 128-383 of lanes 0-15, so only the two T half-slots
 // of lanes 16-31 remain; P' is BF16 (8 KB per slot).
+#ifndef SNAPMLA_SPF
+#define SNAPMLA_SPF 1   // FP8 kernel: S(n+1) TMEM load issued before block n's P' stores
+#endif
 template <bool kBf> struct Variant;
 template <> struct Variant<false> {
   static constexpr int kSlots = 5, kTSlots = 3, kBoxes = 4;
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float tt[32];
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t st = n % V::kSlots, ss = n % kSSlots, ps = n % kPSlots;
-        if (j == u.k0 || kBf) {
+        if (j == u.k0 || kBf || !SNAPMLA_SPF) {
           mbar_wait(BAR(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
           tc_fence_after();
           tmem_ld_16x32bx2_x32<32>(tmem_S + lane_off + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
         // prefetch S(n+1) (FP8 only: with the BF16 variant's 2-slot ring it ties P'(n) to the TMA
         // of block n+1 and serialises the pipeline, measured 4x slower per block)
-        if (!kBf && j + 1 < u.k1) {
+        if (!kBf && SNAPMLA_SPF && j + 1 < u.k1) {
           const uint32_t ss1 = (n + 1) % kSSlots;
           mbar_wait(BAR(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
           tc_fence_after();
