@@ -132,8 +132,29 @@ def logits(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale):
 # --------------------------------------------------------------------------
 # O7: closed form of the SnapMLA decode (the parity gate)
 # --------------------------------------------------------------------------
+def p_quant_mx(w, group):
+    """NEXT-4(b) variant (NOT the paper's method): MX-style power-of-two P scales, one per
+    (row, `group` tokens) as a UE8M0 shared exponent (OCP MX format, the operand format of
+    B200's kind::mxf8f6f4.block_scale).  The paper quantizes with sigma_p = M/448 per 64-token
+    block; here sigma_g = 2^ceil(log2(M_g / 448)), so M_g / sigma_g lies in (224, 448]
+    and one bit of headroom is lost at worst.  Returns A = sigma_g * dec(E4M3(w / sigma_g))
+    (0 for a group whose max is 0)."""
+    w = np.asarray(w, dtype=np.float64)
+    A = np.zeros_like(w)
+    for start in range(0, w.shape[1], group):
+        sl = slice(start, min(start + group, w.shape[1]))
+        wb = w[:, sl]
+        M = wb.max(axis=1)
+        e = np.ceil(np.log2(np.where(M > 0, M, 1.0) / E4M3_MAX))
+        sig = np.ldexp(1.0, e.astype(np.int64))
+        pd = decode_e4m3(encode_e4m3((wb / sig[:, None]).astype(np.float32)))
+        pd[M == 0] = 0.0
+        A[:, sl] = sig[:, None] * pd
+    return A
+
+
 def decode_o7(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale,
-              block=B_C, p_quant=True, block_range=None):
+              block=B_C, p_quant=True, block_range=None, p_mx_group=None):
     """Closed form of Algorithm 1 for one request.
 
       w[r,j]   = exp(s[r,j] - m[r]) * sigma_K[j]          scale fusion, Alg.1 step 6
@@ -154,6 +175,8 @@ def decode_o7(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale,
     ``block_range=(b0, b1)`` restricts to key blocks [b0, b1) (one split-KV
     partial, combined by ``combine``).  ``p_quant=False`` replaces the P
     rounding by the identity (then O7 == O6 up to fp64 rounding).
+    ``p_mx_group=g`` replaces the paper's P quantization by the NEXT-4(b) MX
+    variant (``p_quant_mx``, power-of-two scale per g tokens) -- not the method.
 
     Returns (o [H,512] fp64, lse [H] fp64, natural log).
     """
@@ -166,7 +189,9 @@ def decode_o7(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale,
     e = np.exp(s - m[:, None])
     w = e * np.asarray(sk[j0:j1], dtype=np.float64)[None, :]
     A = np.zeros_like(w)              # A[r,j] = (M[r,b]/448) dec(P'[r,j])
-    for start in range(0, j1 - j0, block):
+    if p_mx_group is not None:
+        A = p_quant_mx(w, p_mx_group)
+    for start in (range(0, j1 - j0, block) if p_mx_group is None else ()):
         sl = slice(start, min(start + block, j1 - j0))
         wb = w[:, sl]
         M = wb.max(axis=1)

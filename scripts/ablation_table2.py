@@ -6,6 +6,8 @@ attention output vs the BF16 ground truth (O8, fp64 over the unquantized inputs)
 RMSE, cosine difference, relative L2.  Rows:
   snapmla_kv / A / B / C / D   exact softmax over the dequantized cache (KV-only)
   snapmla_full                 the full SnapMLA decode (O7: + Q quant, + block P quant)
+  full_mx32 / full_mx64        NEXT-4(b) variant: the same with MX power-of-two P scales per
+                               32 / 64 tokens instead of sigma_p = M/448 (not the method)
   python scripts/ablation_table2.py [context] [heads] [n_layers] > profiles/...json
 """
 import json
@@ -45,10 +47,14 @@ for li in range(N_LAYERS):
     o7, _ = O.decode_o7(qc, sq, qr, kc, sk, kr, SCALE)
     m = O.error_metrics(o7, o8)
     row["snapmla_full"] = {k: m[k] for k in ("rmse", "cos_diff", "rel_l2")}
+    for g in (32, 64):
+        om, _ = O.decode_o7(qc, sq, qr, kc, sk, kr, SCALE, p_mx_group=g)
+        m = O.error_metrics(om, o8)
+        row[f"full_mx{g}"] = {k: m[k] for k in ("rmse", "cos_diff", "rel_l2")}
     layers.append(row)
 
 summary = {}
-for cfg in CONFIGS + ["snapmla_full"]:
+for cfg in CONFIGS + ["snapmla_full", "full_mx32", "full_mx64"]:
     summary[cfg] = {k: float(np.mean([lay[cfg][k] for lay in layers])) for k in ("rmse", "cos_diff", "rel_l2")}
 print(json.dumps({"what": "Table 2 configurations vs BF16 ground truth (O8), synthetic MLA-like caches",
                   "context": L, "heads": H, "layers": N_LAYERS, "softmax_scale": SCALE,

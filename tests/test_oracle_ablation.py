@@ -1,5 +1,6 @@
 """Pins of the Table-2 KV quantization configurations (NEXT-4(a), P:413-429;
 granularities of Appendix A)."""
+import pytest
 import numpy as np
 import torch
 
@@ -66,3 +67,50 @@ def test_attn_dequantized_identity_is_o8():
     o2, l2 = O.attn_o8(q, c, r, 0.07)
     np.testing.assert_allclose(o1, o2, rtol=1e-13, atol=1e-15)
     np.testing.assert_allclose(l1, l2, rtol=1e-13)
+
+
+# ---- NEXT-4(b): MX-style power-of-two P scales (a variant, not the method)
+@pytest.mark.parametrize("group", [32, 64])
+def test_p_quant_mx_vs_torch_cast(group):
+    """p_quant_mx against torch's own E4M3 cast (an independent implementation): per (row,
+    group) the scale is the power of two 2^ceil(log2(max / 448)) and the codes are
+    float8_e4m3fn(w / scale)."""
+    rng = np.random.default_rng(group)
+    w = rng.exponential(size=(7, 150)) * np.exp(rng.normal(size=(7, 1)) * 3)
+    w[2, 40:80] = 0.0   # an all-zero group
+    A = O.p_quant_mx(w, group)
+    for r in range(w.shape[0]):
+        for g0 in range(0, w.shape[1], group):
+            blk = w[r, g0:g0 + group]
+            M = blk.max()
+            if M == 0:
+                assert np.all(A[r, g0:g0 + group] == 0)
+                continue
+            sig = 2.0 ** np.ceil(np.log2(M / 448.0))
+            assert M / 448.0 <= sig < 2 * M / 448.0
+            ref = torch.from_numpy((blk / sig).astype(np.float32)).to(torch.float8_e4m3fn).double().numpy() * sig
+            np.testing.assert_array_equal(A[r, g0:g0 + group], ref)
+
+
+def test_mx_variant_loses_the_exact_block_max():
+    """Why the paper's sigma_p = M/448 matters: it maps each block's largest weight to
+    448, which E4M3 represents exactly, so the dominant term of a peaked softmax is exact.  A
+    power-of-two MX scale leaves M/sigma in (224, 448], rounded to 3 mantissa bits.  Both stay
+    within the E4M3 bound (relative 2^-4 per weight), but on MLA-like logits the MX decode
+    error is far larger than the paper's."""
+    rng = np.random.default_rng(5)
+    c, r = synth.latent_tokens(rng, 700)
+    q = synth.queries(rng, 8)
+    kc, sk, kr = O.append_quant(c.float().numpy(), r.float().numpy())
+    qc, sq, qr = O.q_quant(q.float().numpy())
+    s = O.logits(qc, sq, qr, kc, sk, kr, 0.07)
+    w = np.exp(s - s.max(axis=1, keepdims=True)) * sk[None, :].astype(np.float64)
+    A = O.p_quant_mx(w, 32)
+    big = w > 2.0 ** -6 * w.max()            # normal range of E4M3 after scaling
+    assert (np.abs(A - w) / w)[big].max() <= 2.0 ** -4
+    o_id, _ = O.decode_o7(qc, sq, qr, kc, sk, kr, 0.07, p_quant=False)
+    o_p, _ = O.decode_o7(qc, sq, qr, kc, sk, kr, 0.07)
+    o_mx, _ = O.decode_o7(qc, sq, qr, kc, sk, kr, 0.07, p_mx_group=32)
+    e_p = O.error_metrics(o_p, o_id)["rel_l2"]
+    e_mx = O.error_metrics(o_mx, o_id)["rel_l2"]
+    assert e_p < 1e-3 and e_mx > 10 * e_p and e_mx < 0.1
