@@ -76,7 +76,7 @@ def test_seq_len_sweep(L):
     _check(Case([L], 16, seed=L))
 
 
-@pytest.mark.parametrize("H", [16, 32, 64, 128])
+@pytest.mark.parametrize("H", [1, 8, 16, 32, 63, 64, 100, 128])
 def test_head_counts(H):
     _check(Case([700, 64, 1, 2049], H, seed=H))
 
