@@ -6,7 +6,7 @@ import numpy as np
 import torch
 from paper_2602_10718_b200 import ops, synth
 
-B, H, L = 64, 128, 32768
+B, H, L = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (64, 128, 32768)))
 dev = torch.device("cuda")
 gen = torch.Generator(device=dev); gen.manual_seed(0)
 ppr = L // 64
@@ -40,3 +40,13 @@ def med(a, b):
 print("QKkvq-TMA", med(0, 9), "QK-QKkvq", med(9, 1), "SM_in-QK", med(1, 4), "SMsc-SM_in", med(4, 8),
       "SMsoft-SMsc", med(8, 10), "SMpemp-SMsoft", med(10, 11), "SM_out-SMpemp", med(11, 5),
       "PVpp-SM_out", med(5, 12), "PV_L-PVpp", med(12, 2), "C0-SM_out", med(5, 13), "C_L-PV_L", med(2, 6), "C_R-C_L", med(6, 7))
+
+ct = tr.cpu().numpy()[16 * 256:].reshape(-1, 2).astype(np.int64)
+ok = ct[:, 0] > 0
+if ok.any():
+    d = (ct[ok, 1] - ct[ok, 0]) / 1e3
+    print("CTA durations us: min/median/max", d.min(), np.median(d), d.max(), "span", (ct[ok, 1].max() - ct[ok, 0].min()) / 1e3)
+rel = t - t[0][0]
+print("first blocks (TMA, QK, PV_L, SM_in, SM_out, C_L):")
+for n in range(min(nv, 6)):
+    print(n, [int(rel[e][n]) for e in (0, 1, 2, 4, 5, 6)])
