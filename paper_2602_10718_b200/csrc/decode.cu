@@ -226,6 +226,12 @@ __device__ __forceinline__ float div_by(float x, float s, float rs) {
   const float q = x * rs;
   return fmaf(fmaf(-q, s, x), rs, q);
 }
+// the same on a pair, packed f32x2 (bit-identical to two div_by calls: fma(q, -s, x) == fma(-q, s, x))
+__device__ __forceinline__ float2 div_by2(float2 x, float s, float rs) {
+  const float2 rs2 = make_float2(rs, rs), ns2 = make_float2(-s, -s);
+  const float2 q = __fmul2_rn(x, rs2);
+  return __ffma2_rn(__ffma2_rn(q, ns2, x), rs2, q);
+}
 
 // One QK block into S (TMEM): 16 x kind::f8f6f4 (K = 32) over the 512 content dims,
 // then 4 x kind::f16 (K = 16) over the 64 RoPE dims, accumulating into the same S;
@@ -571,8 +577,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                                         div_by(f1.y, sq, rsq));
+              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
+              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
             }
           }
           tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
@@ -1756,8 +1762,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              qa[4 * g8 + e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                                         div_by(f1.y, sq, rsq));
+              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
+              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
             }
           }
           tmem_st_32x32b_x32(tmem + lane_base + k2TmemQ + 32 * cc, qa);
