@@ -1472,7 +1472,7 @@ constexpr uint32_t kIdescPvS = make_idesc(0, 0, 0, 1, 128, 256);
 constexpr uint32_t k2TmemQ = 64, k2TmemT = 192;
 
 struct Bars2 {
-  alignas(16) uint8_t sink[kPSlots][16];   // landing bytes of the peer's P' signal (bulk-copy aligned)
+  alignas(16) uint8_t sink[kPSlots + 1][16];   // landing bytes of the peer's P' / Q signals (bulk-copy aligned)
   uint64_t kv_full[k2Slots];    // leader: Kq + RoPE + V of both CTAs (cta_group::2 TMA)
   uint64_t sc_full[k2Slots];    // local: sigma_K of the block
   uint64_t kv_empty[k2Slots];   // PV_L + PV_R commits (multicast)
@@ -1482,6 +1482,7 @@ struct Bars2 {
   uint64_t q_full, q_free;
   uint32_t tmem_base;
   float crow[64];
+  float xa[2][64];              // Q-quant prologue: partial amax of each accumulator column group
   float xm[2][2][64];           // [block parity][token half][row] partial max of t
   float xl[2][2][64], xw[2][2][64];   // partial l and max of w
   float stat[kPSlots][3][64];
@@ -1559,7 +1560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(B2(t_full) + 8 * i, 1);
       mbar_init(B2(t_free) + 8 * i, leader ? 8 + 1 : 8);   // leader: 8 local warps + the peer's forward; peer: local
     }
-    mbar_init(B2(q_full), 8);                  // the 4 prologue warps of both CTAs
+    mbar_init(B2(q_full), leader ? 12 + 1 : 12);   // 8 acc + 4 softmax local warps (+ the peer's forward)
     mbar_init(B2(q_free), 1);
     fence_barrier_init();
   }
@@ -1664,8 +1665,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ======== peer: forward "S slot read" (its 4 softmax warps, local barrier) to the leader ========
       // (remote arrives issued by the compute warps themselves stall them; measured)
       const uint32_t s_empty_leader = mapa_shared(B2(s_empty), 0);
-      uint32_t n = 0;
+      const uint32_t q_full_leader = mapa_shared(B2(q_full), 0);
+      uint32_t n = 0, unit = 0;
       while (it.next(u)) {
+        // this CTA's Q (codes in TMEM, q_r' in SMEM) -> the leader's QK: 16-byte bulk copy
+        // completing the leader's q_full after the local q_full (acquire) of all 12 writers
+        mbar_wait(B2(q_full), unit & 1, 18, unit);
+        tc_fence_after();
+        if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(B2(sink), 0) + 16 * kPSlots, sbase + k2OffQr);
+        __syncwarp();
+        ++unit;
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t ss = n % kSSlots;
           mbar_wait(B2(s_empty) + 8 * ss, (n / kSSlots) & 1, 16, n);
@@ -1726,71 +1735,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // per N half: rows for the CTA-0 token half from lanes 0-63, for the CTA-1 half from
       // lanes 64-127 (measured: scripts/exp/dbg_2sm_s.py), so every warp writes the codes
       // of its 32 rows into its own lane quarter; SMSPs 0-1 also write q_r' and c.
+      // The 512 q codes of a row are computed by the two accumulator warps of the row's SMSP
+      // (256 each, written into that SMSP's TMEM lane quarter); the softmax warp combines their
+      // partial amax into sigma_q and writes q_r' / sigma_q and c (SMSPs 0-1).
       if (unit > 0) {
         mbar_wait(B2(q_free), (unit - 1) & 1, 11, unit);
         named_bar_sync(1, 128);
       }
+      named_bar_sync(4, 384);   // partial amax of the accumulator warps written
       {
-        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-        float amax = 0.f;
-        for (int c8 = 0; c8 < 64; c8 += 8) {
-          uint4 qv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + c8 + i) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(hv[e]);
-              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-            }
-          }
-        }
+        const float amax = fmaxf(lds_f32(B2(xa) + 4 * r), lds_f32(B2(xa) + 256 + 4 * r));
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
-        if (hk == 0) sts_f32(B2(crow) + 4 * r, sq * p.scale_log2);
-#pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {     // 128 codes = 32 TMEM columns per store
-          uint32_t qa[32];
+        if (hk == 0) {
+          const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
+          sts_f32(B2(crow) + 4 * r, sq * p.scale_log2);
 #pragma unroll
-          for (int g8 = 0; g8 < 8; ++g8) {
-            uint4 v2[2];
-            v2[0] = row_ok ? __ldg(qrow + 16 * cc + 2 * g8) : make_uint4(0, 0, 0, 0);
-            v2[1] = row_ok ? __ldg(qrow + 16 * cc + 2 * g8 + 1) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
+            uint32_t wd[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
-              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
+              const float2 f = __bfloat1622float2(a[e]);
+              __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
+                                                     __float2bfloat16_rn(div_by(f.y, sq, rsq)));
+              wd[e] = *reinterpret_cast<uint32_t*>(&o2);
             }
+            sts_u4(sbase + k2OffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
           }
-          tmem_st_32x32b_x32(tmem + lane_base + k2TmemQ + 32 * cc, qa);
-        }
-        tmem_wait_st();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (hk) break;
-          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-          uint32_t wd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(a[e]);
-            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
-          }
-          sts_u4(sbase + k2OffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
         }
         fence_proxy_async_smem();
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(B2(q_full));
-          else mbar_arrive_cluster(q_full_leader);
-        }
+        if (lane == 0) mbar_arrive(B2(q_full));   // local (the peer's warp 9 forwards it)
       }
       named_bar_sync(1, 128);
       const float c_row = lds_f32(B2(crow) + 4 * r);
@@ -1923,8 +1900,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int dbase = (k >> 1) * 256 + 64 * cg;   // T_L column c -> dim dbase + c; T_R -> + 128
     const uint32_t stat0 = B2(stat) + 4 * r;
     const uint32_t t_free_leader = mapa_shared(B2(t_free), 0);
-    uint32_t n = 0;
+    uint32_t n = 0, unit = 0;
     while (it.next(u)) {
+      // ---- Q-quant prologue share: codes [256 cg, 256 cg + 256) of row r into this SMSP's lanes
+      if (unit > 0) mbar_wait(B2(q_free), (unit - 1) & 1, 19, unit);
+      {
+        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk) + 32 * cg;
+        float amax = 0.f;
+#pragma unroll 1
+        for (int c8 = 0; c8 < 32; c8 += 8) {
+          uint4 qv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + c8 + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(hv[e]);
+              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+            }
+          }
+        }
+        sts_f32(B2(xa) + 256 * cg + 4 * r, amax);
+        named_bar_sync(4, 384);
+        const float am = fmaxf(lds_f32(B2(xa) + 4 * r), lds_f32(B2(xa) + 256 + 4 * r));
+        const float sq = fmaxf(__fdiv_rn(am, 448.0f), kSigmaMin);
+        const float rsq = __frcp_rn(sq);
+#pragma unroll 1
+        for (int ci = 0; ci < 2; ++ci) {   // 128 codes = 32 TMEM columns per store
+          uint32_t qa[32];
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            uint4 v2[2];
+            v2[0] = row_ok ? __ldg(qrow + 16 * ci + 2 * g8) : make_uint4(0, 0, 0, 0);
+            v2[1] = row_ok ? __ldg(qrow + 16 * ci + 2 * g8 + 1) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
+              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
+            }
+          }
+          tmem_st_32x32b_x32(tmem + lane_base + k2TmemQ + 32 * (2 * cg + ci), qa);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B2(q_full));
+      }
+      ++unit;
       const uint32_t n0 = n;
       float o[128];
 #pragma unroll
