@@ -219,6 +219,13 @@ struct UnitIter {
 };
 
 
+// The TMA producer's page-id loads are a dependent chain (each TMA needs its block-table entry);
+// at a unit start they would cost one DRAM round trip per block (~2K cycles, CTA-0 timeline),
+// so the unit's block-table segment is requested up front, one L1 prefetch per 128-byte line.
+__device__ __forceinline__ void prefetch_block_table(const int32_t* bt, int k0, int k1) {
+  for (int j = k0 & ~31; j < k1; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(bt + j));
+}
+
 // ------------------------------------------------------------- decode kernel
 // x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
@@ -428,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t n = 0;
         while (it.next(u)) {
           const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          prefetch_block_table(bt, u.k0, u.k1);
           for (int j = u.k0; j < u.k1; ++j, ++n) {
             const uint32_t st = n % V::kSlots;
             mbar_wait_backoff(BAR(kv_empty) + 8 * st, ((n / V::kSlots) & 1) ^ 1);
@@ -1596,6 +1604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t n = 0;
         while (it.next(u)) {
           const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
+          prefetch_block_table(bt, u.k0, u.k1);
           for (int j = u.k0; j < u.k1; ++j, ++n) {
             const uint32_t st = n % k2Slots;
             mbar_wait_backoff(B2(kv_empty) + 8 * st, ((n / k2Slots) & 1) ^ 1);
