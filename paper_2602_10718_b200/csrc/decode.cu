@@ -7,7 +7,7 @@
 //
 // B200 design: one persistent CTA per SM, one 64-row query-head
 // tile per CTA (UMMA M = 64), split-KV over 64-token key blocks planned on the
-// device, a 4-slot ring of KV blocks in SMEM.  Warp roles (16 warps; the SM
+// device, a 5-slot ring of KV blocks in SMEM.  Warp roles (16 warps; the SM
 // schedulers prefer the highest eligible warp id, so latency-critical roles get
 // the high ids):
 //   warps 0-7    two accumulator warpgroups (O columns 0-255 / 256-511): the
@@ -33,10 +33,12 @@
 // merge, and the debug timeline compiled out of production builds.
 // Each block's softmax is computed against its OWN max (the P' codes depend only
 // on w / max_block(w)); the accumulator warps carry the running max.
-// TMEM (512 cols): lanes 0-15 of each 32-lane subpartition hold T slots 0 / 1
-// (cols 0-255 / 256-511); lanes 16-31 hold four S slots (cols 64 s) and T slot 2
-// (cols 256-511).  PV half h = 2n + (0: L, 1: R) goes to T slot h % 3, so PV(n+1)
+// TMEM map: see t_slot_addr (lanes 0-15: S slots, the q_c codes, T slot 0; lanes 16-31:
+// T slots 1 / 2).  PV half h = 2n + (0: L, 1: R) goes to T slot h % 3, so PV(n+1)
 // overlaps the accumulation of block n.
+// The same kernel templated on kBf is the BF16 baseline (NEXT-2, Variant<true>); the
+// experimental CTA-pair kernels for 64 < rows <= 128 (mla_decode_pair_kernel,
+// mla_decode_2sm_kernel) follow below it.
 #include "snapmla_internal.h"
 
 namespace snapmla {
