@@ -53,6 +53,17 @@ def parse():
     ap.add_argument("--context", type=int, default=None)
     ap.add_argument("--heads", type=int, default=None)
     ap.add_argument("--mode", default="dp", choices=["dp", "tp", "dptp"])
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="dp: 'weak' = the workload's batch on every rank, 'strong' = the workload's batch is the "
+                         "GLOBAL batch split over the ranks (dist.dp_range); auto = strong for longcat (BASELINE "
+                         "configs[3]), weak otherwise")
+    ap.add_argument("--no-peaks", action="store_true", help="skip the on-box FP8 GEMM / read-stream peak measurement")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "bp"],
+                    help="64 < rows <= 128: force the single-CTA or the block-pair kernel (experiments; "
+                         "default: the library's automatic choice)")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="launch the ranks, print every rank's partition and the max-over-ranks reduction, exit "
+                         "(no GPU work; exercises the launcher / partition / reduction path)")
     ap.add_argument("--tp", type=int, default=2, help="--mode dptp: TP group size (world = DP x TP)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="tp / dptp: all-gather fused into the combine epilogue (mla_combine_gather, symmetric memory)")
@@ -71,6 +82,173 @@ def parse():
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` run without a launcher: re-exec this command as N ranks of one node
+    (torch.distributed.run, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_dist(world, local_rank):
+    """One process per GPU, NCCL.  With more ranks than visible GPUs (a 1-GPU box checking
+    the N-rank path) ranks share devices round-robin and the control plane (barrier,
+    max-over-ranks timing) runs on gloo; those numbers are marked "oversubscribed"."""
+    import torch
+    import torch.distributed as dist
+    ndev = max(torch.cuda.device_count(), 1)
+    dev_idx = local_rank % ndev
+    oversub = world > ndev or not torch.cuda.is_available()
+    if world > 1:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(dev_idx)
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+    return dev_idx, oversub
+
+
+def allreduce_max(vals, dev, oversub):
+    """max over ranks of a list of floats (CUDA tensor on NCCL, CPU tensor on gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return list(vals)
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if oversub else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def measure_peaks(dev, lib):
+    """On-box roofline denominators measured in this run: FP8 dense GEMM
+    (torch._scaled_mm, cuBLASLt, 8192^3 E4M3 -> BF16) burst (best single launch of 10) and
+    sustained (back to back for 2 s), and a read-only HBM stream (our measurement kernel,
+    mla_measure_read_stream over 4 GiB, best of 10)."""
+    import ctypes
+    import torch
+    out = {}
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn)
+        b = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=dev, dtype=torch.float32)
+
+        def mm():
+            return torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        for _ in range(3):
+            mm()
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            mm()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out["fp8_tflops_burst"] = round(2 * n ** 3 / (best / 1e3) / 1e12, 1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cnt, t_start = 0, time.time()
+        e0.record()
+        while time.time() - t_start < 2.0:
+            for _ in range(20):
+                mm()
+            cnt += 20
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        out["fp8_tflops_sustained"] = round(2 * n ** 3 * cnt / (e0.elapsed_time(e1) / 1e3) / 1e12, 1)
+        del a, b
+    except Exception as ex:   # noqa: BLE001 -- a missing FP8 GEMM leaves the tensor roof on the fallback
+        out["fp8_error"] = f"{type(ex).__name__}: {ex}"[:200]
+    try:
+        nbytes = 4 << 30
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        sink = torch.zeros(4096, dtype=torch.int64, device=dev)
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        f = lib.mla_measure_read_stream
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        for _ in range(2):
+            assert f(ctypes.c_void_p(buf.data_ptr()), nbytes, ctypes.c_void_p(sink.data_ptr()), 4096, stream) == 0
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f(ctypes.c_void_p(buf.data_ptr()), nbytes, ctypes.c_void_p(sink.data_ptr()), 4096, stream)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out["read_gbs"] = round(nbytes / (best / 1e3) / 1e9, 1)
+        del buf, sink
+    except Exception as ex:   # noqa: BLE001
+        out["read_error"] = f"{type(ex).__name__}: {ex}"[:200]
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_info():
+    """CPU model, usable cores and the BLAS thread pools numpy will use."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = []
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()]
+    except Exception:   # noqa: BLE001
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)), "blas": blas,
+            "blas_threads": max([b["threads"] or 0 for b in blas], default=None)}
+
+
+def rank_plan(args, world, rank):
+    """What rank `rank` of `world` runs (pure host logic, tested on CPU with gloo): its requests
+    (DP weak: the workload's batch per replica; DP strong: dist.dp_range of the global batch),
+    its heads (TP: dist.tp_range) and the tokens of the whole job per step."""
+    from paper_2602_10718_b200 import dist as D
+    w = workload(args)
+    B, H = w["batch"], w["heads"]
+    tp_world, t_idx, d_idx = 1, 0, rank
+    if args.mode == "tp":
+        tp_world, t_idx, d_idx = world, rank, 0
+    elif args.mode == "dptp":
+        tp_world = args.tp
+        d_idx, t_idx = D.dptp_coords(world, tp_world, rank)
+    n_dp = world // tp_world
+    strong = scaling_mode(args) == "strong"
+    r0, r1 = D.dp_range(B, n_dp, d_idx) if strong else (0, B)
+    head0, head1 = D.tp_range(H, tp_world, t_idx)
+    return {"rank": rank, "world": world, "dp": n_dp, "tp": tp_world, "d_idx": d_idx, "t_idx": t_idx,
+            "requests": [r0, r1], "batch": r1 - r0, "global_batch": B if strong else B * n_dp,
+            "heads": [head0, head1], "scaling": scaling_mode(args),
+            "tokens_per_step": (B if strong else B * n_dp) * args.mtp}
+
+
+def scaling_mode(args):
+    if args.mode == "tp":
+        return "strong"
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong" if args.workload == "longcat" else "weak"
 
 
 def workload(args):
@@ -133,13 +311,60 @@ def measured_peaks():
 
 
 def ncu_traffic(workload_key):
-    """dram bytes per decode launch from the committed ncu --set full summary, or None."""
+    """(dram bytes per decode launch, provenance) from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     d = json.load(open(p))
     e = d.get(workload_key)
-    return None if e is None else e.get("dram_bytes_per_launch")
+    if e is None:
+        return None, None
+    return e.get("dram_bytes_per_launch"), {k: e.get(k) for k in ("round", "commit", "kernel", "dram_pct_peak",
+                                                                   "tensor_pipe_active_pct")}
+
+
+SPEC_HBM_GBS, SPEC_FP8_TFLOPS, SPEC_BF16_TFLOPS = 8000.0, 4500.0, 2250.0
+
+
+def roofline_record(dec_bytes, flops, dec_ms, peaks, bf16, kernel, dec_stats, workload_key, mtp):
+    """Both roofs of the decode launch: t_hbm = algorithmic bytes / HBM peak and
+    t_tc = FP8-equivalent flops / FP8 dense peak; `bound` is the larger, `frac` = t_roof / t."""
+    hbm_peak, hbm_src = measured_peaks()
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    if bf16:
+        tc_peak = mp.get("bf16_tflops_sustained")
+        tc_src = "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, sustained)"
+        tc_burst, tc_spec = mp.get("bf16_tflops"), SPEC_BF16_TFLOPS
+    elif peaks.get("fp8_tflops_sustained"):
+        tc_peak = peaks["fp8_tflops_sustained"]
+        tc_src = "measured in this run: torch._scaled_mm FP8 E4M3 8192^3, back to back for 2 s (sustained)"
+        tc_burst, tc_spec = peaks.get("fp8_tflops_burst"), SPEC_FP8_TFLOPS
+    else:
+        tc_peak = 2 * mp.get("bf16_tflops_sustained", 1403.4)
+        tc_src = "fallback: MEASURED_PEAKS.json bf16 sustained x 2 (nominal FP8 / BF16 ratio)"
+        tc_burst, tc_spec = None, SPEC_FP8_TFLOPS
+    t = dec_ms / 1e3
+    t_hbm, t_tc = dec_bytes / (hbm_peak * 1e9), flops / (tc_peak * 1e12)
+    a_hbm, a_tc = dec_bytes / t / 1e9, flops / t / 1e12
+    rb = peaks.get("read_gbs")
+    hbm = {"achieved": round(a_hbm, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(a_hbm / hbm_peak, 4),
+           "t_roof_ms": round(t_hbm * 1e3, 4), "peak_source": hbm_src, "frac_spec_8TBs": round(a_hbm / SPEC_HBM_GBS, 4),
+           "read_stream_gbs": rb, "frac_read_stream": round(a_hbm / rb, 4) if rb else None}
+    tensor = {"achieved": round(a_tc, 1), "peak": tc_peak, "unit": "TFLOP/s", "frac": round(a_tc / tc_peak, 4),
+              "t_roof_ms": round(t_tc * 1e3, 4), "peak_source": tc_src, "peak_burst": tc_burst,
+              "frac_spec": round(a_tc / tc_spec, 4),
+              "flops_per_unit": ("2176 BF16 flop" if bf16 else "2304 FP8-equivalent flop (QK content 2x512 + PV 2x512 "
+                                 "at the FP8 rate, QK RoPE 2x64 at half the rate)") + " per (query row, cached token)"}
+    bound = "tensor" if t_tc > t_hbm else "hbm"
+    b = tensor if bound == "tensor" else hbm
+    traffic, tsrc = ncu_traffic(workload_key) if mtp == 1 and not bf16 else (None, None)
+    return {"bound": bound, "kernel": kernel, "achieved": b["achieved"], "peak": b["peak"], "unit": b["unit"],
+            "frac": b["frac"], "traffic": traffic, "traffic_source": tsrc,
+            "binding_margin": round(max(t_hbm, t_tc) / min(t_hbm, t_tc), 3),
+            "decode_ms": round(dec_ms, 4), "decode_ms_stats": dec_stats,
+            "algorithmic_bytes_per_launch": dec_bytes, "flops_per_launch": flops,
+            "roofs": {"hbm": hbm, "tensor": tensor}}
 
 
 # ------------------------------------------------------------- our arm
@@ -150,24 +375,23 @@ def run_ours(args, rank, world, local_rank):
     from paper_2602_10718_b200 import dist as D
     from paper_2602_10718_b200 import ops, synth
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_idx, oversub = getattr(args, "dev_idx", local_rank), getattr(args, "oversub", False)
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     w = workload(args)
-    B, H, L = w["batch"], w["heads"], w["context"]
+    H, L = w["heads"], w["context"]
     T = args.mtp
-    # head partition: TP over the whole world, or over consecutive-rank TP groups (DP x TP)
-    tp_world, t_idx, d_idx, tp_group = 1, 0, rank, None
-    if args.mode == "tp":
-        tp_world, t_idx, d_idx = world, rank, 0
-    elif args.mode == "dptp":
-        tp_world = args.tp
-        d_idx, t_idx = D.dptp_coords(world, tp_world, rank)
-        tp_group = D.dptp_groups(world, tp_world) if world > 1 else None
-    n_dp = world // tp_world
-    head0, head1 = D.tp_range(H, tp_world, t_idx)
+    plan = rank_plan(args, world, rank)   # requests / heads of this rank (tested on CPU: tests/test_bench_launch.py)
+    B, B_global, n_dp, tp_world = plan["batch"], plan["global_batch"], plan["dp"], plan["tp"]
+    d_idx, t_idx = plan["d_idx"], plan["t_idx"]
+    head0, head1 = plan["heads"]
+    tp_group = D.dptp_groups(world, tp_world) if args.mode == "dptp" and world > 1 else None
     heads_local = head1 - head0
     scale = synth.DEFAULT_SOFTMAX_SCALE
 
+    if args.kernel != "auto":
+        ops.lib().mla_debug_set_pair({"single": 0, "bp": 1}[args.kernel])
+    peaks = {} if (args.quick or args.no_peaks) else measure_peaks(dev, ops.lib())
     gen = torch.Generator(device=dev)
     # TP replicas hold identical KV; DP ranks hold their own requests
     gen.manual_seed(1234 + d_idx)   # the ranks of one TP group hold identical KV
@@ -208,22 +432,30 @@ def run_ours(args, rank, world, local_rank):
             ops.mla_decode_bf16(qx, cache.kv_c, cache.kv_rope, block_table, seq_lens, scale, ws)
         else:
             decode_fp8(qx, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
-    gathered, peer_ptrs = None, None
+    gathered, peer_ptrs, sym = None, None, None
     if tp_world > 1 and args.fused_gather:
         if T > 1:
             raise SystemExit("--fused-gather supports mtp = 1")
-        gathered, peer_ptrs = D.symmetric_gather_output((B, H, 512), tp_group or dist.group.WORLD, dev)
+        if oversub:
+            raise SystemExit("--fused-gather needs one GPU per rank (peer memory)")
+        # two symmetric output buffers alternated by step parity: rank r's gather of step i+1
+        # must not overwrite rank j's step-i output while rank j still reads it (snapmla.h)
+        sym = [D.symmetric_gather_output((B, H, 512), tp_group or dist.group.WORLD, dev) for _ in range(2)]
+        gathered, peer_ptrs = sym[0]
     elif tp_world > 1:
         gathered = torch.empty(tp_world, B, heads_local, 512, dtype=torch.bfloat16, device=dev)
 
     if peer_ptrs is not None:
         out = gathered[:, head0:head1]   # this rank's heads of the gathered result (e2e read-back)
+    gather_step = [0]
 
-    def combine_and_gather(out_t=None, lse_t=None):
+    def combine_and_gather(out_t=None, lse_t=None, parity=None):
         out_t = out if out_t is None else out_t
         lse_t = lse if lse_t is None else lse_t
         if peer_ptrs is not None:   # NEXT-4(c): peer stores from the combine epilogue + stream barrier
-            ops.mla_combine_gather(ws, B, rows, peer_ptrs, t_idx, lse_t)
+            k = gather_step[0] % 2 if parity is None else parity
+            gather_step[0] += 1
+            ops.mla_combine_gather(ws, B, rows, sym[k][1], t_idx, lse_t)
             D.stream_barrier(tp_group, dev)
             return
         ops.mla_combine(ws, B, rows, out_t, lse_t)
@@ -235,9 +467,13 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ev_d0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_d1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_s0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_s1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
     def step(i=None):
         # a1: the T new tokens of every request land at positions L-T .. L-1 (same slots each step)
+        if i is not None:
+            ev_s0[i].record(stream)
         for t in range(T):
             cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         if i is not None:
@@ -246,8 +482,10 @@ def run_ours(args, rank, world, local_rank):
         if i is not None:
             ev_d1[i].record(stream)
         combine_and_gather()
+        if i is not None:
+            ev_s1[i].record(stream)
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev_idx)
     clocks.start()
     for _ in range(max(3, args.warmup)):
         step()
@@ -269,30 +507,34 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # per-launch decode time for the roofline: a second pass of the same steps with events
-    # around each decode (plan + decode launches) on the launching stream
+    # per-launch decode time for the roofline and the per-step distribution: a second pass of
+    # the same steps with events around each step and each decode (plan + decode launches) on
+    # the launching stream (never between the plan and the PDL-launched decode)
     for i in range(args.steps):
         step(i)
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    dec_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_d0, ev_d1)]))
-    if world > 1:
-        t = torch.tensor([ms, dec_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, dec_ms = float(t[0]), float(t[1])
+    dec_all = [a.elapsed_time(b) for a, b in zip(ev_d0, ev_d1)]
+    step_all = [a.elapsed_time(b) for a, b in zip(ev_s0, ev_s1)]
+    stats = [float(np.mean(dec_all))] + [float(np.percentile(x, q)) for x in (dec_all, step_all) for q in (50, 10, 90)]
+    ms, *stats = allreduce_max([ms] + stats, dev, oversub)
+    dec_ms = stats[0]
+    dec_stats = {"median": round(stats[1], 4), "p10": round(stats[2], 4), "p90": round(stats[3], 4)}
+    step_stats = {"median": round(stats[4], 4), "p10": round(stats[5], 4), "p90": round(stats[6], 4)}
     ms_step = ms / args.steps
 
     peak, peak_src = measured_peaks()
     bytes_per_token = 2 * (512 + 64) if args.bf16 else BYTES_PER_TOKEN
     kv_bytes = B * L * bytes_per_token
     dec_bytes = kv_bytes + B * rows * 576 * 2       # algorithmic bytes per decode launch
+    flops = B * L * rows * (2176 if args.bf16 else 2304)   # FP8-equivalent (BF16 for the baseline) per launch
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9
-    tokens_per_step = B * T * n_dp
+    tokens_per_step = B_global * T
     if args.quick:
         return {"metric": METRIC, "value": round(tokens_per_step / (ms_step / 1e3), 1),
                 "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True,
-                "batch": B, "heads": H, "context": L, "mtp": T,
+                "batch": B, "global_batch": B_global, "heads": H, "context": L, "mtp": T, "n_gpus": world,
                 "roofline_frac": round(achieved / peak, 4), "achieved_gbs": round(achieved, 1), "clocks": clk}
 
     # ---------------- e2e: host buffers through the public API
@@ -326,11 +568,7 @@ def run_ours(args, rank, world, local_rank):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t[0])
+    e_ms = allreduce_max([e0.elapsed_time(e1)], dev, oversub)[0]
     h2d = q_h.numel() * 2 + c_h.numel() * 2 + r_h.numel() * 2
     d2h = out_h.numel() * 2 + lse_h.numel() * 4
 
@@ -340,7 +578,8 @@ def run_ours(args, rank, world, local_rank):
     # inside the timed region
     cp_s, rb_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     din = [(torch.empty_like(q), torch.empty_like(new_c), torch.empty_like(new_r)) for _ in range(2)]
-    dout = [(torch.empty_like(out) if peer_ptrs is None else out, torch.empty_like(lse)) for _ in range(2)]
+    dout = [(torch.empty_like(out) if peer_ptrs is None else sym[k][0][:, head0:head1], torch.empty_like(lse))
+            for k in range(2)]
     hout = [(torch.empty(out.shape, dtype=out.dtype).pin_memory(), torch.empty(lse.shape, dtype=lse.dtype).pin_memory())
             for _ in range(2)]
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -366,7 +605,7 @@ def run_ours(args, rank, world, local_rank):
             cache.append(new_cr[t][0], new_cr[t][1], block_table, seq_lens_t[t])
         cache.append(cd, rd, block_table, seq_lens)
         decode(qd)
-        combine_and_gather(dout[k][0], dout[k][1])
+        combine_and_gather(dout[k][0], dout[k][1], parity=k)
         ev_comp[k].record(stream)
 
     def d2h_issue(i):
@@ -389,6 +628,8 @@ def run_ours(args, rank, world, local_rank):
 
     pipelined(3)
     torch.cuda.synchronize()
+    clocks_e2e = ClockSampler(dev_idx)
+    clocks_e2e.start()
     t_settle = time.time()
     while time.time() - t_settle < 1.0:   # same power / clock state as the device-timed loop (sw_power_cap)
         pipelined(10)
@@ -401,11 +642,8 @@ def run_ours(args, rank, world, local_rank):
     pipelined(args.steps)
     p1.record(stream)
     torch.cuda.synchronize()
-    p_ms = p0.elapsed_time(p1)
-    if world > 1:
-        t = torch.tensor([p_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        p_ms = float(t[0])
+    p_ms = allreduce_max([p0.elapsed_time(p1)], dev, oversub)[0]
+    clk_e2e = clocks_e2e.stop()
 
     value = tokens_per_step / (ms_step / 1e3)
     launches_per_step = T + 3   # append x T, plan, decode, combine (all ours)
@@ -418,23 +656,23 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "strong" if args.mode == "tp" else "weak",
+        "scaling": scaling_mode(args),
         "vs_baseline": None,
         "dtype": "bf16 (NEXT-2 unquantized baseline; f32 accumulate)" if args.bf16 else "fp8e4m3 (f32 accumulate; bf16 RoPE)",
         "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
         "config": {
-            "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else ""), "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
+            "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else ""), "global_batch": B_global,
+            "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
             "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": T,
             "parallelism": f"dp{n_dp}tp{tp_world}" + ("+fused-gather" if peer_ptrs is not None else ""),
+            "ranks_per_gpu": "oversubscribed (ranks share GPUs; gloo control plane)" if oversub else 1,
             "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
         },
-        "roofline": {
-            "bound": "hbm", "kernel": ("mla_decode_bf16" if args.bf16 else "mla_decode_fp8") + " (plan + decode launches)",
-            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(args.workload) if T == 1 and not args.bf16 else None, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": dec_bytes, "decode_ms": round(dec_ms, 4),
-            "bytes_per_unit": f"{bytes_per_token} B per cached token + 1152 B per (request, query token, head) q row",
-        },
+        "roofline": roofline_record(dec_bytes, flops, dec_ms, peaks, args.bf16,
+                                    ("mla_decode_bf16" if args.bf16 else "mla_decode_fp8") + " (plan + decode launches)",
+                                    dec_stats, args.workload, T)
+        | {"bytes_per_unit": f"{bytes_per_token} B per cached token + 1152 B per (request, query token, head) q row"},
+        "ms_per_step_stats": step_stats,
         "e2e": {"value": round(tokens_per_step / (p_ms / args.steps / 1e3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "mode": "pipelined: H2D of step i+1 (pinned host -> device, copy stream) and D2H of step i "
@@ -442,6 +680,8 @@ def run_ours(args, rank, world, local_rank):
                 "serial_value": round(tokens_per_step / (e_ms / args.steps / 1e3), 1)},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
+        "clocks_e2e": clk_e2e,
+        "peaks_measured": peaks,
     }
     return res
 
@@ -491,11 +731,11 @@ def cpu_baseline(args, budget_s):
         oracle_only_decode(kc2, sk2, kr2, q, synth.DEFAULT_SOFTMAX_SCALE)
         t_tot += time.perf_counter() - t
         n += 1
-    cores = len(os.sched_getaffinity(0))
-    return {"value": round(n / t_tot, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+    ci = cpu_info()
+    return {"value": round(n / t_tot, 4), "unit": "tokens/s", "cores": ci["cores"], "kind": "oracle",
             "sample": f"{n} whole requests of the workload ({H} heads x {L} context): append of the new "
                       f"token + q-quant + O7 closed-form decode + combine, numpy fp64, {t_tot:.1f} s",
-            "threads": cores}
+            "threads": ci["blas_threads"], "cpu_model": ci["cpu_model"], "blas": ci["blas"]}
 
 
 def run_reference(args):
@@ -519,7 +759,8 @@ def run_reference(args):
         one()
     dt = time.perf_counter() - t
     value = args.steps / dt      # one decode token (request) per step
-    cores = len(os.sched_getaffinity(0))
+    ci = cpu_info()
+    cores = ci["cores"]
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
@@ -527,7 +768,8 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": w["name"], "batch_per_rank": w["batch"], "heads": H,
                                         "context": L, "page": 64, "parallelism": "cpu"},
         "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"each step = 1 whole request ({H} heads x {L} context) of the workload"},
+                         "sample": f"each step = 1 whole request ({H} heads x {L} context) of the workload",
+                         "threads": ci["blas_threads"], "cpu_model": ci["cpu_model"]},
         "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -614,17 +856,29 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args)))
         return
-    if world > 1:
-        import torch
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    args.dev_idx, args.oversub = init_dist(world, local_rank)
+    if args.plan_only:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        plan = rank_plan(args, world, rank)
+        plans = [plan]
+        if world > 1:
+            plans = [None] * world
+            dist.all_gather_object(plans, plan)
+        tmax = allreduce_max([float(rank + 1)], None, True)[0]
+        if rank == 0:
+            print(json.dumps({"n_gpus": world, "plans": plans, "max_over_ranks_check": tmax}))
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if args.sweep:
         run_sweep(args, rank, world, local_rank)
         return
     if args.fetch:
         if rank == 0:
-            print(json.dumps(run_fetch(args, local_rank)))
+            print(json.dumps(run_fetch(args, args.dev_idx)))
         return
     res = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick and not args.bf16:

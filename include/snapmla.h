@@ -31,6 +31,18 @@
  *     that reads them.
  *   - Deterministic: identical inputs on the same GPU give bitwise identical
  *     outputs (no atomics in reductions).
+ *   - Thread safety: every call may be made concurrently from several host
+ *     threads, on any streams and devices (the current device of the calling
+ *     thread is used).  The only process-wide state is (a) per-device launch
+ *     records (SM count, dynamic-SMEM attributes, cluster occupancy) set once,
+ *     (b) a 32-entry cache of encoded TMA tensor maps keyed by (device, pool
+ *     base, pool rows, kind) -- a pool freed and re-allocated at the same
+ *     address with the same extent reuses a map that is still valid -- both
+ *     under one mutex, and (c) the debug switches of snapmla_debug.h (atomics).
+ *   - Kernel choice (mla_decode_fp8 / _ex, 64 < q_len x heads <= 128): the
+ *     block-pair 2-SM kernel when batch x max_pages_per_seq >= 16384 (the
+ *     block table's extent bounds the work; seq_lens stay on the device), else
+ *     the single-CTA kernel.  Both compute the same closed form (O7).
  */
 #ifndef SNAPMLA_H_
 #define SNAPMLA_H_
@@ -147,6 +159,10 @@ mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* k
  *   out  bf16 [batch, num_heads, kv_lora_rank]  (RNE from fp32)
  *   lse  fp32 [batch, num_heads], natural log; may be NULL
  * A request with seq_lens[b] == 0 yields out = 0 and lse = -inf.
+ * The workspace must come from a decode with the same batch and num_heads (rows: q_len x
+ * heads for MTP) on a device with the same SM count: the decode's plan header records
+ * them and the combine kernel traps (the stream's context reports an error) on a mismatch
+ * instead of reading partials at the wrong offsets.
  */
 mla_status mla_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out, float* lse,
                        mla_stream_t stream);
@@ -206,6 +222,10 @@ mla_status mla_decode_bf16(const void* q, const void* kv_c, const void* kv_rope,
  *   lse           fp32 [batch, num_heads] of this rank's heads (local), may be NULL.
  * The stores are plain P2P writes: the caller orders them before any consumer on another
  * rank with a stream-ordered barrier (e.g. a one-element NCCL all-reduce) after this call.
+ * Write-after-read: rank r's NEXT gather may overwrite rank j's output while rank j still
+ * reads the previous step's rows, so successive steps must alternate between two output
+ * buffers (step parity; bench.py --fused-gather does) or put a stream-ordered barrier
+ * BEFORE this call as well.
  */
 mla_status mla_combine_gather(const void* workspace, int batch, int num_heads, int kv_lora_rank,
                               void* const* out_peers, int world, int rank, float* lse, mla_stream_t stream);

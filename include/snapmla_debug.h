@@ -3,6 +3,7 @@
  */
 #ifndef SNAPMLA_DEBUG_H_
 #define SNAPMLA_DEBUG_H_
+#include <stddef.h>
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -13,15 +14,16 @@ extern "C" {
  * CTA's n-th key block.  NULL disables it (default). */
 void mla_debug_set_trace(unsigned long long* dev_buf);
 /* Kernel for decodes with 64 < rows <= 128 (e.g. 128 heads): v = 0 the single-CTA
- * kernel (two independent M = 64 CTAs per key range; the default),
- * v = 2 the 2-SM kernel (cta_group::2 QK and PV with token / dims halves per CTA of
- * a cluster pair; §7.8), v = 1 the CTA-pair kernel (cta_group::2 QK over two key
- * blocks, per-CTA PV; §7.6).  v = 1, 2 are experimental.  Process-global. */
+ * kernel (two independent M = 64 CTAs per key range), v = 2 the 2-SM
+ * kernel (cta_group::2 QK and PV with token / dims halves per CTA of a cluster pair;
+ * §7.8), v = 3 the block-pair 2-SM kernel (§7.9).  Process-global. */
 void mla_debug_set_pair(int v);
-/* Cap the number of CTA pairs the pair kernel launches (0 = as many as fit);
- * returns the cudaOccupancyMaxActiveClusters limit seen on the last pair launch
- * (-1 before the first).  For measurements only. */
-int mla_debug_set_pair_groups(int v);
+/* Measurement only (bench.py's roofline denominator): a read-only stream over
+ * [buf, buf + bytes) (device memory, 16-B aligned, bytes % 16 == 0), one XOR
+ * fold per CTA into sink[0 .. min(sink_len, 4 x SMs)) (device memory, zeroed by
+ * the caller).  Enqueued on `stream`; returns an mla_status. */
+int mla_measure_read_stream(const void* buf, size_t bytes, unsigned long long* sink, int sink_len,
+                            void* stream);
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) append_quant_kernel(const __nv_bfloat16* 
                                                            int max_pages, uint8_t* __restrict__ kv_fp8,
                                                            __nv_bfloat16* __restrict__ kv_rope,
                                                            float* __restrict__ kv_scale) {
+  pdl_launch_dependents();   // the decode's plan may start now (it reads no append output)
   const int lane = threadIdx.x & 31;
   const int tok = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (tok >= batch) return;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(256) append_bf16_kernel(const uint4* __restric
                                                           const int32_t* __restrict__ seq_lens, int batch,
                                                           int max_pages, uint4* __restrict__ kv_c,
                                                           uint4* __restrict__ kv_rope) {
+  pdl_launch_dependents();   // the decode's plan may start now (it reads no append output)
   const int lane = threadIdx.x & 31;
   const int tok = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (tok >= batch) return;

@@ -19,14 +19,20 @@ struct Peers {
 
 template <bool kF32Out, bool kGather = false>
 __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ ws, size_t off_cum, size_t off_lse,
-                                                      size_t off_o, int batch, int num_heads,
+                                                      size_t off_o, int batch, int num_heads, int num_sms,
                                                       void* __restrict__ out, float* __restrict__ lse_out,
                                                       const Peers peers = Peers{}) {
+  pdl_wait();   // launched as a programmatic dependent of the decode: its partials are complete here
   const int lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (idx >= batch * num_heads) return;
   const int b = idx / num_heads, h = idx % num_heads;
   const int32_t* hdr = reinterpret_cast<const int32_t*>(ws);
+  // The workspace must come from a decode of the same shape on a device with the same SM
+  // count (the partial offsets depend on them, snapmla.h): a mismatch -- e.g. heads passed
+  // instead of q_len x heads for MTP, another batch, another device -- traps loudly instead
+  // of reading out of bounds.
+  if (hdr[H_BATCH] != batch || hdr[H_HEADS] != num_heads || hdr[H_SMS] != num_sms) __trap();
   const int32_t* cum = reinterpret_cast<const int32_t*>(ws + off_cum);
   const float* lse_p = reinterpret_cast<const float*>(ws + off_lse);
   const float* o_p = reinterpret_cast<const float*>(ws + off_o);
@@ -94,6 +100,21 @@ __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ w
   if (lse_out && lane == 0) lse_out[idx] = lse;
 }
 
+// programmatic dependent launch (the kernel's griddepcontrol.wait orders it after the decode)
+template <typename... KArgs, typename... Args>
+static mla_status launch_pdl(void (*kernel)(KArgs...), int grid, mla_stream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...) == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}
+
 template <bool kF32>
 static mla_status launch_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out,
                                  float* lse, mla_stream_t stream) {
@@ -108,9 +129,8 @@ static mla_status launch_combine(const void* workspace, int batch, int num_heads
   if (sms <= 0) return MLA_ERR_CUDA;
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   const int n = batch * num_heads;
-  combine_kernel<kF32><<<(n + 3) / 4, 128, 0, (cudaStream_t)stream>>>(
-      static_cast<const char*>(workspace), wl.cum, wl.lse, wl.o, batch, num_heads, out, lse);
-  return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+  return launch_pdl(combine_kernel<kF32>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum, wl.lse,
+                    wl.o, batch, num_heads, sms, out, lse, Peers{});
 }
 
 }  // namespace snapmla
@@ -140,9 +160,8 @@ extern "C" mla_status mla_combine_gather(const void* workspace, int batch, int n
   if (sms <= 0) return MLA_ERR_CUDA;
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   const int n = batch * num_heads;
-  combine_kernel<false, true><<<(n + 3) / 4, 128, 0, (cudaStream_t)stream>>>(
-      static_cast<const char*>(workspace), wl.cum, wl.lse, wl.o, batch, num_heads, nullptr, lse, peers);
-  return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+  return launch_pdl(combine_kernel<false, true>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum,
+                    wl.lse, wl.o, batch, num_heads, sms, static_cast<void*>(nullptr), lse, peers);
 }
 
 extern "C" mla_status mla_combine(const void* workspace, int batch, int num_heads, int kv_lora_rank, void* out,

@@ -39,6 +39,9 @@
 // The same kernel templated on kBf is the BF16 baseline (NEXT-2, Variant<true>); the
 // experimental CTA-pair kernels for 64 < rows <= 128 (mla_decode_pair_kernel,
 // mla_decode_2sm_kernel) follow below it.
+#include <atomic>
+#include <mutex>
+
 #include "snapmla_internal.h"
 
 namespace snapmla {
@@ -125,7 +128,8 @@ static_assert(sizeof(Bars) <= 4096, "barrier region");
 // test_block_aligned_split_plus_combine_equals_unsplit).
 __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ seq_lens, int batch, int num_heads,
                                                     int groups, int32_t* __restrict__ hdr,
-                                                    int32_t* __restrict__ cum, int32_t* __restrict__ first_req) {
+                                                    int32_t* __restrict__ cum, int32_t* __restrict__ first_req,
+                                                    int num_sms) {
   __shared__ int warp_sums[32];
   __shared__ int s_per;
   const int tid = threadIdx.x;
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
     hdr[H_NHT] = (num_heads + kHeadTile - 1) / kHeadTile;
     hdr[H_BATCH] = batch;
     hdr[H_HEADS] = num_heads;
+    hdr[H_SMS] = num_sms;   // the SM count the workspace layout was computed with (combine checks it)
   }
   __syncthreads();
   const int per = s_per;
@@ -192,6 +197,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
     const int c1 = c0 + (L > 0 ? (L + kBc - 1) / kBc : 0);
     for (int g = (c0 + per - 1) / per; g < groups && g * per < c1; ++g) first_req[g] = b;
   }
+  // launched as a programmatic dependent of the append: complete only after it, so the
+  // decode's griddepcontrol.wait (on this grid) also orders its cache reads after the append
+  pdl_wait();
 }
 
 // ------------------------------------------------------------------- units
@@ -411,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_S = tmem;                       // lanes 0-15 (+32k): S slot s at cols 64 s
 
   pdl_wait();   // plan (and the appends before it) visible from here on
+  pdl_launch_dependents();   // the combine may be scheduled as CTAs retire (it waits for completion)
   const int ht = blockIdx.x % p.n_ht;
   const int g = blockIdx.x / p.n_ht;
   const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
@@ -860,669 +869,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 }
 
-// ===================================================================== CTA-pair kernel
-// 64 < rows <= 128 (DeepSeek-R1's 128 heads): the two head tiles of a key range run as
-// a CTA pair (cluster of 2) and share the QK tensor work through cta_group::2 MMAs.
-// Measured data path (scripts/pair_probe.cu): for cta_group::2, M = 128 (64 rows per CTA),
-// CTA c holds D[row r, col n] at lane r for n < N/2 (B columns supplied by CTA 0) and at
-// lane 64 + r, column n - N/2 for n >= N/2 (B columns supplied by CTA 1).  So one pair QK
-// of N = 128 over TWO key blocks -- block A from CTA 0's SMEM, block B from CTA 1's -- leaves
-// every CTA with S(A) for its 64 rows on lanes 0-63 and S(B) on lanes 64-127: the softmax of
-// block A runs on SMSPs 0-1 and that of block B on SMSPs 2-3, one thread per (row, block)
-// with all 64 tokens in-thread (no shuffles).  The QK costs 32 instead of 64 cycles per
-// 32-byte K chunk per block (tcgen05 floor max(M,128) N / (256 cta_group)).
-// PV stays per CTA (cta_group::1, M = 64, P' x V of its own rows; mixing both groups in one
-// kernel is validated by the same probe) into 6 quarter tiles (64 x 128) of TMEM.
-// Pair SMEM slot = two 41 KB sub-slots; CTA 0 keeps block A in sub-slot 0, CTA 1 keeps
-// block B there, so the leader's QK operand address is the same in both CTAs.
-// Cross-CTA traffic per block pair: the peer's sub-slot-0 TMA completes on the leader's
-// barrier (cta_group::2 TMA), the peer's four softmax warps arrive (relaxed) on the
-// leader's s_empty, and the QK commit multicasts s_full to both CTAs.  Once per unit the
-// peer's Q-quant prologue arrives (release) on the leader's q_full.
-constexpr int kPairSlots = 2;                        // KV ring depth (block pairs)
-constexpr int kPrefetchPairs = 2;                    // L2 prefetch distance (block pairs)
-constexpr int kQSlots = 6;                           // TMEM ring of 64 x 128 PV quarter tiles
-constexpr uint32_t kPairStage = 2 * kStage;          // two blocks
-constexpr uint32_t kPOffQc = 0;                      // q_c codes: 4 SW128 boxes [64 rows x 128 B]
-constexpr uint32_t kPOffQr = 32768;                  // q_r / sigma_q (BF16, SW128)
-constexpr uint32_t kPOffP = 40960;                   // P' 2 slots x 4096
-constexpr uint32_t kPOffKv = 49152;
-constexpr uint32_t kPOffBar = kPOffKv + kPairSlots * kPairStage;
-constexpr uint32_t kPSmemBytes = kPOffBar + 4096 + 1024;
-static_assert(kPSmemBytes <= 232448, "shared memory budget (pair kernel)");
-constexpr uint32_t kTxSub0 = 4 * kBoxBytes + kBoxBytes;   // content + RoPE of one block (QK operand)
-constexpr uint32_t kIdescQk8P = make_idesc(0, 0, 0, 0, 128, 128);
-constexpr uint32_t kIdescQk16P = make_idesc(1, 1, 0, 0, 128, 128);
-constexpr uint32_t kIdescPvQ = make_idesc(0, 0, 0, 1, 64, 128);
-// registers (setmaxnreg, per SMSP 2 acc + 1 issue + 1 softmax warp): the pair softmax holds a
-// whole 64-token row per thread, the accumulators read T in 8-column chunks
-constexpr uint32_t kPRegsAcc = 168, kPRegsSoftmax = 136;
-static_assert(2 * 32 * kPRegsAcc + 32 * kRegsIssue + 32 * kPRegsSoftmax <= 4 * 32 * 128, "pair register budget");
-
-struct PairBars {
-  uint64_t kvq_full[kPairSlots];   // sub-slot 0 of both CTAs landed (leader)
-  uint64_t kvl_full[kPairSlots];   // sub-slot 1 content of this CTA landed
-  uint64_t sc_full[kPairSlots];    // sigma_K of both blocks landed (loaded first: the softmax needs only these)
-  uint64_t kv_empty[kPairSlots];   // PV_L + PV_R of the pair's last block completed
-  uint64_t s_full[kSSlots], s_empty[kSSlots];
-  uint64_t p_full[kPSlots], p_empty[kPSlots];
-  uint64_t t_full[kQSlots], t_free[kQSlots];
-  uint64_t q_full, q_free;
-  uint32_t tmem_base;
-  float crow[64];
-  float stat[kPSlots][3][64];
-};
-static_assert(sizeof(PairBars) <= 4096, "barrier region (pair kernel)");
-#define PBAR(field) (bar0 + (uint32_t)offsetof(PairBars, field))
-
-// One pair QK (leader only): S[ss] (+)= q_c x K_c^T (16 x K = 32, A and B from SMEM)
-// + q_r' x K_r'^T (4 x K = 16), cta_group::2, M = 128, N = 128; commit multicast to both CTAs.
-#define SNAPMLA_QK8P(o, acc)                                                                   \
-  "add.s64 a, %1, " #o ";\n\tadd.s64 b, %2, " #o ";\n\t"                                       \
-  "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], a, b, %3, " acc ";\n\t"
-#define SNAPMLA_QK16P(o)                                                                       \
-  "add.s64 a, %4, " #o ";\n\tadd.s64 b, %5, " #o ";\n\t"                                       \
-  "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %6, pt;\n\t"
-__device__ __forceinline__ void qk_issue_pair(uint32_t dS, uint64_t dQc, uint64_t dK, uint64_t dQr, uint64_t dKr,
-                                              uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
-      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      SNAPMLA_QK8P(0, "pf") SNAPMLA_QK8P(2, "pt") SNAPMLA_QK8P(4, "pt") SNAPMLA_QK8P(6, "pt")
-      SNAPMLA_QK8P(512, "pt") SNAPMLA_QK8P(514, "pt") SNAPMLA_QK8P(516, "pt") SNAPMLA_QK8P(518, "pt")
-      SNAPMLA_QK8P(1024, "pt") SNAPMLA_QK8P(1026, "pt") SNAPMLA_QK8P(1028, "pt") SNAPMLA_QK8P(1030, "pt")
-      SNAPMLA_QK8P(1536, "pt") SNAPMLA_QK8P(1538, "pt") SNAPMLA_QK8P(1540, "pt") SNAPMLA_QK8P(1542, "pt")
-      SNAPMLA_QK16P(0) SNAPMLA_QK16P(2) SNAPMLA_QK16P(4) SNAPMLA_QK16P(6)
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %8;\n\t}"
-      ::"r"(dS), "l"(dQc), "l"(dK), "r"(kIdescQk8P), "l"(dQr), "l"(dKr), "r"(kIdescQk16P), "r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
-
-// One PV quarter (cta_group::1): T = P' (64 x 64 tokens, K-major) x V (64 tokens x 128 dims,
-// MN-major), 2 x K = 32; commit to t_full.
-__device__ __forceinline__ void pv_issue_quarter(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t) {
-  asm volatile(
-      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
-      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
-      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
-      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPvQ), "r"(bar_t)
-      : "memory");
-}
-
-// TMEM (pair kernel): S pair slots at cols 64 ss (all 128 lanes); PV quarter slot s at
-// lane group 16 (s & 1) (M = 64 layout), cols 128 + 128 (s >> 1).
-__device__ __forceinline__ uint32_t q_slot_addr(uint32_t tmem, uint32_t s) {
-  return tmem + ((s & 1u) ? (16u << 16) : 0u) + 128u + 128u * (s >> 1);
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    mla_decode_pair_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
-                           const DecodeParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar0 = sbase + kPOffBar;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t cta = cluster_ctarank();   // == head tile
-  const bool leader = cta == 0;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kPairSlots; ++i) {
-      mbar_init(PBAR(kvq_full) + 8 * i, 1);
-      mbar_init(PBAR(kvl_full) + 8 * i, 1);
-      mbar_init(PBAR(sc_full) + 8 * i, 1);
-      mbar_init(PBAR(kv_empty) + 8 * i, 2);
-    }
-    for (int i = 0; i < kSSlots; ++i) {
-      mbar_init(PBAR(s_full) + 8 * i, 1);
-      mbar_init(PBAR(s_empty) + 8 * i, 8);      // 4 local + 4 peer softmax warps (leader's copy is used)
-    }
-    for (int i = 0; i < kPSlots; ++i) {
-      mbar_init(PBAR(p_full) + 8 * i, 2);       // the two softmax warps of the block's parity
-      mbar_init(PBAR(p_empty) + 8 * i, 2 + 8);  // PV_L + PV_R commits, 8 accumulator warps
-    }
-    for (int i = 0; i < kQSlots; ++i) {
-      mbar_init(PBAR(t_full) + 8 * i, 1);
-      mbar_init(PBAR(t_free) + 8 * i, 4);
-    }
-    mbar_init(PBAR(q_full), 8);                 // 4 local + 4 peer prologue warps
-    mbar_init(PBAR(q_free), 1);
-    fence_barrier_init();
-  }
-  if (warp == kWarpTma && lane == 0) {
-    tma_prefetch_desc(&tm_kv);
-    tma_prefetch_desc(&tm_rope);
-  }
-  if (warp == kWarpQk) tmem_alloc_pair(PBAR(tmem_base), 512);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();   // peer barriers initialised before any remote arrive / TMA completion
-  tc_fence_after();
-  const uint32_t tmem = lds_u32(PBAR(tmem_base));
-
-  pdl_wait();
-  const int ht = (int)cta;
-  const int g = blockIdx.x / 2;
-  const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
-  const int lo = g * per;
-  const bool has_work = g < groups && lo < total;
-  const int hi = min(total, lo + per);
-#ifdef SNAPMLA_TRACE
-  if (p.trace != nullptr && threadIdx.x == 0) {
-    unsigned long long gt;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x] = gt;
-  }
-#endif
-  UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
-  Unit u;
-  // sub-slot of block A (k0 + 2i) / B (k0 + 2i + 1) in this CTA
-  const uint32_t subA = leader ? 0u : 1u;
-
-  if (warp >= kWarpTma && warp < kWarpSoftmax) {
-    regs_dec<kRegsIssue>();
-    if (warp == kWarpTma) {
-      // ============================ TMA producer (per block pair) ============================
-      if (lane == 0) {
-        const uint64_t pol = l2_policy_evict_first();
-        const uint32_t kvq_leader0 = mapa_shared(PBAR(kvq_full), 0);
-        uint32_t np = 0;
-        while (it.next(u)) {
-          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
-          for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
-            const bool hasB = jA + 1 < u.k1;
-            const uint32_t st = np % kPairSlots;
-            mbar_wait_backoff(PBAR(kv_empty) + 8 * st, ((np / kPairSlots) & 1) ^ 1);
-            TRACE(TR_TMA, np);
-            const uint32_t slot = sbase + kPOffKv + st * kPairStage;
-            const int rowA = __ldg(bt + jA) * kPage;
-            const int rowB = hasB ? __ldg(bt + jA + 1) * kPage : 0;
-            // L2 prefetch kPrefetchPairs pairs ahead (this CTA: its sub-slot-0 block), so the
-            // TMA of a recycled slot hits L2 instead of waiting a full DRAM round trip
-            {
-              const int jp = jA + 2 * kPrefetchPairs + (leader ? 0 : 1);
-              if (jA == u.k0) {   // unit start: the first pairs too
-                for (int jj = jA + 2 + (leader ? 0 : 1); jj < min(jp, u.k1); jj += 2) {
-                  const int64_t rp = (int64_t)__ldg(bt + jj) * kPage;
-                  bulk_prefetch_l2(p.kv_fp8 + rp * kDc, kPage * kDc);
-                  bulk_prefetch_l2(p.kv_rope + rp * kDr, kPage * kDr * 2);
-                }
-              }
-              if (jp < u.k1) {
-                const int64_t rp = (int64_t)__ldg(bt + jp) * kPage;
-                bulk_prefetch_l2(p.kv_fp8 + rp * kDc, kPage * kDc);
-                bulk_prefetch_l2(p.kv_rope + rp * kDr, kPage * kDr * 2);
-              }
-            }
-            // sub-slot 0: the QK operand (leader: block A, peer: block B), counted on the leader's barrier
-            if (leader) mbar_arrive_expect_tx(PBAR(kvq_full) + 8 * st, kTxSub0 * (hasB ? 2u : 1u));
-            // scales first (local): the softmax waits only for these
-            const uint32_t sc_bar = PBAR(sc_full) + 8 * st;
-            const uint32_t sA = slot + subA * kStage, sB = slot + (1u - subA) * kStage;
-            mbar_arrive_expect_tx(sc_bar, 256u * (hasB ? 2u : 1u));
-            bulk_load(sA + 5 * kBoxBytes, p.kv_scale + (int64_t)rowA, 128, sc_bar, pol);
-            bulk_load(sA + kOffScaleHi, p.kv_scale + (int64_t)rowA + 32, 128, sc_bar, pol);
-            if (hasB) {
-              bulk_load(sB + 5 * kBoxBytes, p.kv_scale + (int64_t)rowB, 128, sc_bar, pol);
-              bulk_load(sB + kOffScaleHi, p.kv_scale + (int64_t)rowB + 32, 128, sc_bar, pol);
-            }
-            const int row0 = leader ? rowA : rowB;
-            const uint32_t q_bar = kvq_leader0 + 8 * st;
-            if (leader || hasB) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) tma_load_2d_cg2(slot + c * kBoxBytes, &tm_kv, q_bar, c * 128, row0, pol);
-              tma_load_2d_cg2(slot + 4 * kBoxBytes, &tm_rope, q_bar, 0, row0, pol);
-            }
-            // local: sub-slot 1 content (the other block's V)
-            const bool has1 = leader ? hasB : true;
-            const int row1 = leader ? rowB : rowA;
-            const uint32_t l_bar = PBAR(kvl_full) + 8 * st;
-            mbar_arrive_expect_tx(l_bar, has1 ? 4 * kBoxBytes : 0u);   // armed every pair (phase = pair count)
-            if (has1) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                tma_load_2d(slot + kStage + c * kBoxBytes, &tm_kv, l_bar, c * 128, row1, pol);
-            }
-          }
-        }
-      }
-    } else if (warp == kWarpQk) {
-      // ================================ pair QK issuer (leader) ================================
-      if (leader) {
-        const uint64_t dQc = make_smem_desc(sbase + kPOffQc, 16, 1024, LAYOUT_SW128);
-        const uint64_t dQr = make_smem_desc(sbase + kPOffQr, 16, 1024, LAYOUT_SW128);
-        uint32_t np = 0, unit = 0;
-        while (it.next(u)) {
-          mbar_wait(PBAR(q_full), unit & 1, 2, unit);
-          for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
-            const uint32_t st = np % kPairSlots, ss = np % kSSlots;
-            mbar_wait(PBAR(kvq_full) + 8 * st, (np / kPairSlots) & 1, 3, np);
-            if (lane == 0) TRACE(TR_S2, np);
-            mbar_wait(PBAR(s_empty) + 8 * ss, ((np / kSSlots) & 1) ^ 1, 4, np);
-            tc_fence_after();
-            if (lane == 0) TRACE(TR_QK, np);
-            const uint32_t kv = sbase + kPOffKv + st * kPairStage;
-            qk_issue_pair(tmem + 64 * ss, dQc, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
-                          make_smem_desc(kv + 4 * kBoxBytes, 16, 1024, LAYOUT_SW128), PBAR(s_full) + 8 * ss);
-          }
-          mma_commit_pair_ws(PBAR(q_free));   // both CTAs' Q reusable once this unit's QK completed
-          ++unit;
-        }
-      }
-    } else {
-      // ============================ PV_L / PV_R (per CTA, quarters) ============================
-      const uint32_t half = warp - kWarpPv;
-      uint32_t n = 0, np = 0;
-      while (it.next(u)) {
-        for (int jA = u.k0; jA < u.k1; jA += 2, ++np) {
-          const int nb = jA + 1 < u.k1 ? 2 : 1;
-          const uint32_t st = np % kPairSlots;
-          for (int b = 0; b < nb; ++b, ++n) {
-            const uint32_t ps = n % kPSlots;
-            mbar_wait(PBAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
-            if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
-            const uint32_t pA = sbase + kPOffP + ps * 4096;
-            const uint32_t sub = b == 0 ? subA : 1u - subA;
-            if (sub == 1) mbar_wait(PBAR(kvl_full) + 8 * st, (np / kPairSlots) & 1, 13, n);   // V of sub-slot 1
-            const uint32_t vb = sbase + kPOffKv + st * kPairStage + sub * kStage + (2 * half) * kBoxBytes;
-#pragma unroll
-            for (int qi = 0; qi < 2; ++qi) {
-              const uint32_t q = 4 * n + 2 * half + qi, qs = q % kQSlots;
-              if (q >= kQSlots) mbar_wait(PBAR(t_free) + 8 * qs, (q / kQSlots - 1) & 1, 6, n);
-              tc_fence_after();
-              pv_issue_quarter(q_slot_addr(tmem, qs), make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
-                               make_smem_desc(vb + qi * kBoxBytes, kBoxBytes, 1024, LAYOUT_SW128),
-                               PBAR(t_full) + 8 * qs);
-            }
-            mma_commit_ws(PBAR(p_empty) + 8 * ps);
-            if (b == nb - 1) mma_commit_ws(PBAR(kv_empty) + 8 * st);
-          }
-        }
-      }
-    }
-  } else if (warp >= kWarpSoftmax) {
-    regs_inc<kPRegsSoftmax>();
-    const int k = warp & 3;
-    // ---- prologue mapping (as the single-CTA kernel): row r = 16k + t, content half hh
-    const int t = lane & 15, hh = lane >> 4;
-    const int r = 16 * k + t;
-    const int head = ht * kHeadTile + r;
-    const bool row_ok = head < p.num_heads;
-    // ---- softmax mapping: block parity par (A: SMSPs 0-1, B: 2-3), row rho, all 64 tokens
-    const int par = k >> 1;
-    const int rho = 32 * (k & 1) + lane;
-    const int head_s = ht * kHeadTile + rho;
-    const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    const uint32_t s_empty_leader = mapa_shared(PBAR(s_empty), 0);
-    const uint32_t q_full_leader = mapa_shared(PBAR(q_full), 0);
-    uint32_t n = 0, np = 0, unit = 0;
-    while (it.next(u)) {
-      // ---------------- Fused-Q-Quant prologue (a2): codes + q_r' into this CTA's SMEM
-      if (unit > 0) {
-        mbar_wait(PBAR(q_free), (unit - 1) & 1, 11, unit);
-        named_bar_sync(1, 128);   // every softmax warp read the previous unit's crow
-      }
-      {
-        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-        float amax = 0.f;
-#pragma unroll
-        for (int bh = 0; bh < 4; ++bh) {
-          uint4 qv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * hh + 8 * bh + i) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(hv[e]);
-              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-            }
-          }
-        }
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
-        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
-        const float rsq = __frcp_rn(sq);
-        if (hh == 0) sts_f32(PBAR(crow) + 4 * r, sq * p.scale_log2);
-        // this thread's 256 content bytes = SW128 boxes 2 hh, 2 hh + 1 of row r
-#pragma unroll
-        for (int half32 = 0; half32 < 2; ++half32) {
-          const uint32_t box = sbase + kPOffQc + (2 * hh + half32) * kBoxBytes + r * 128;
-#pragma unroll
-          for (int g8 = 0; g8 < 8; ++g8) {
-            const int gch = 8 * half32 + g8;
-            uint4 v2[2];
-            v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
-            v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-            uint32_t w4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              w4[e] = cvt4_e4m3(div_by(f0.x, sq, rsq), div_by(f0.y, sq, rsq), div_by(f1.x, sq, rsq),
-                                div_by(f1.y, sq, rsq));
-            }
-            sts_u4(box + ((g8 ^ (r & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
-          }
-        }
-#pragma unroll
-        for (int gch = 0; gch < 4; ++gch) {
-          const int c = 4 * hh + gch;
-          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-          uint32_t wd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(a[e]);
-            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
-          }
-          sts_u4(sbase + kPOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(PBAR(q_full));
-          else mbar_arrive_cluster(q_full_leader);   // release: Q codes published to the leader's MMA
-        }
-      }
-      named_bar_sync(1, 128);   // crow of every row written
-      const float c_row = lds_f32(PBAR(crow) + 4 * rho);
-      const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head_s / p.heads);
-
-      float tt[64];
-      for (int jA = u.k0; jA < u.k1; n += (jA + 1 < u.k1 ? 2 : 1), jA += 2, ++np) {
-        const int nb = jA + 1 < u.k1 ? 2 : 1;
-        const bool mine = par < nb;
-        const uint32_t ss = np % kSSlots, st = np % kPairSlots;
-        mbar_wait(PBAR(s_full) + 8 * ss, (np / kSSlots) & 1, 7, np);
-        tc_fence_after();
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, np);
-        if (threadIdx.x == 32 * kWarpSoftmax + 64) TRACE(TR_S3, np);
-        if (mine) {
-          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
-          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss + 32, *reinterpret_cast<uint32_t(*)[32]>(tt + 32));
-          tmem_wait_ld();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(PBAR(s_empty) + 8 * ss);
-          else mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
-        }
-        if (!mine) continue;
-        const uint32_t nm = n + par, ps = nm % kPSlots;
-        const int j = jA + par;
-        mbar_wait(PBAR(sc_full) + 8 * st, (np / kPairSlots) & 1, 12, np);   // sigma_K landed
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, np);
-        const uint32_t sub = par == 0 ? subA : 1u - subA;
-        const uint32_t skA = sbase + kPOffKv + st * kPairStage + sub * kStage;
-        const int nvalid = L - j * kBc;
-        // Alg.1 step 3 (descale) with sigma_K read from SMEM (broadcast)
-#pragma unroll
-        for (int e = 0; e < 64; e += 4)
-          lds_mul4(skA + (e < 32 ? 5 * kBoxBytes + 4 * e : kOffScaleHi + 4 * (e - 32)), tt[e], tt[e + 1], tt[e + 2],
-                   tt[e + 3]);
-        if (nvalid < 64) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
-        }
-        float m4[4] = {tt[0], tt[1], tt[2], tt[3]};
-#pragma unroll
-        for (int e = 4; e < 64; e += 4) {
-          m4[0] = fmaxf(m4[0], tt[e]);
-          m4[1] = fmaxf(m4[1], tt[e + 1]);
-          m4[2] = fmaxf(m4[2], tt[e + 2]);
-          m4[3] = fmaxf(m4[3], tt[e + 3]);
-        }
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        const float mc = mx == -INFINITY ? 0.f : mx * c_row;
-        float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
-        float mb0 = 0.f, mb1 = 0.f;
-#pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
-          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
-          const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));
-          const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
-          ls0 = __fadd2_rn(ls0, p0);
-          ls1 = __fadd2_rn(ls1, p1);
-          float2 w0 = p0, w1 = p1;
-          lds_mul4(skA + (e < 32 ? 5 * kBoxBytes + 4 * e : kOffScaleHi + 4 * (e - 32)), w0.x, w0.y, w1.x, w1.y);
-          tt[e] = w0.x;
-          tt[e + 1] = w0.y;
-          tt[e + 2] = w1.x;
-          tt[e + 3] = w1.y;
-          mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
-          mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
-        }
-        const float lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
-        const float mb = fmaxf(mb0, mb1);
-        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
-        const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
-        const float2 inv2 = make_float2(inv, inv);
-        uint32_t pw[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
-          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
-          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
-        }
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, np);
-        mbar_wait(PBAR(p_empty) + 8 * ps, ((nm / kPSlots) & 1) ^ 1, 8, nm);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S5, np);
-        const uint32_t sa = PBAR(stat) + ps * (3 * 64 * 4) + 4 * rho;
-        sts_f32(sa, st_m);
-        sts_f32(sa + 256, st_sig);
-        sts_f32(sa + 512, lsum);
-        // K-major core matrices: byte(row, tok) = (tok/16)*1024 + row*16 + tok%16
-        const uint32_t pdst = sbase + kPOffP + ps * 4096 + rho * 16;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sts_u4(pdst + c * 1024, pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(PBAR(p_full) + 8 * ps);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, np);
-        if (threadIdx.x == 32 * kWarpSoftmax + 64) TRACE(TR_C2, np);
-      }
-      ++unit;
-    }
-  } else {
-    regs_inc<kPRegsAcc>();
-    // ========= accumulators: Alg.1 recurrence per row, O <- gamma O + T in registers =========
-    // WG w owns dims [256 w, 256 w + 256) = quarters 2w, 2w+1; thread (row r, hh) holds
-    // dims 256 w + 128 qi + 64 hh + [0, 64) in o[64 qi + ...]
-    const uint32_t w = warp >> 2;
-    const int k = warp & 3;
-    const int t = lane & 15, hh = lane >> 4;
-    const int r = 16 * k + t;
-    const int head = ht * kHeadTile + r;
-    const bool row_ok = head < p.num_heads;
-    const uint32_t lane_off = (uint32_t)(32 * k) << 16;
-    const uint32_t stat0 = PBAR(stat) + 4 * r;
-    uint32_t n = 0;
-    while (it.next(u)) {
-      const uint32_t n0 = n;
-      float o[128];
-#pragma unroll
-      for (int e = 0; e < 128; ++e) o[e] = 0.f;
-      float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
-      for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t ps = n % kPSlots;
-        mbar_wait(PBAR(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
-        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
-        const uint32_t sa = stat0 + ps * (3 * 64 * 4);
-        const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(PBAR(p_empty) + 8 * ps);
-        const float m_new = fmaxf(m_ref, mb);
-        const bool first = n == n0;
-        const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
-        float gamma = 0.f;
-        if (first) {
-          m_O = mb;
-          sig_O = sb;
-          l_run = lb;
-          m_ref = mb;
-        } else if (!skip) {
-          gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);
-          l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
-          m_ref = m_new;
-          m_O = mb;
-          sig_O = sb;
-        }
-        const float2 g2 = make_float2(gamma, gamma);
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-          const uint32_t q = 4 * n + 2 * w + qi, qs = q % kQSlots;
-          mbar_wait(PBAR(t_full) + 8 * qs, (q / kQSlots) & 1, 10, n);
-          tc_fence_after();
-          const uint32_t taddr = q_slot_addr(tmem, qs) + lane_off;
-          uint32_t tv[2][8];
-          tmem_ld_16x32bx2_x8<64>(taddr, tv[0]);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            tmem_wait_ld();
-            if (c < 7) tmem_ld_16x32bx2_x8<64>(taddr + 8 * (c + 1), tv[(c + 1) & 1]);
-            else {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(PBAR(t_free) + 8 * qs);
-            }
-            const uint32_t* cur = tv[c & 1];
-            if (!skip) {
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {
-                const int oi = 64 * qi + 8 * c + e;
-                const float2 a = __ffma2_rn(make_float2(o[oi], o[oi + 1]), g2,
-                                            make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
-                o[oi] = a.x;
-                o[oi + 1] = a.y;
-              }
-            }
-          }
-        }
-        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
-      }
-      const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;
-      (void)0;
-      const int64_t prow = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile + r;
-      if (row_ok) {
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-          float* dst = p.o_part + prow * kDc + 256 * w + 128 * qi + 64 * hh;
-#pragma unroll
-          for (int e = 0; e < 64; e += 4)
-            *reinterpret_cast<float4*>(dst + e) = make_float4(o[64 * qi + e] * f, o[64 * qi + e + 1] * f,
-                                                              o[64 * qi + e + 2] * f, o[64 * qi + e + 3] * f);
-        }
-        if (w == 0 && hh == 0)
-          p.lse_part[prow] = l_run > 0.f ? (m_ref + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
-      }
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();   // the leader's last pair MMAs (into the peer's TMEM) are complete on both sides
-  if (warp == kWarpQk) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem, 512);
-  }
-#ifdef SNAPMLA_TRACE
-  if (p.trace != nullptr && threadIdx.x == 0) {
-    unsigned long long gt;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x + 1] = gt;
-  }
-#endif
-}
-
-// ===================================================================== 2-SM kernel
-// 64 < rows <= 128 as a CTA pair that splits BOTH contractions the way the 2-SM datapath
-// wants (scripts/pair_probe.cu: CTA c holds D[r, n] at lane r for the N/2 columns of CTA 0's
-// B operand and at lane 64 + r for CTA 1's):
-//   QK  cta_group::2, M = 128 (64 rows per CTA), N = 64: CTA c supplies tokens [32c, 32c+32)
-//       of the block (K operand 16 KB + RoPE 4 KB); every CTA gets S for its rows with
-//       tokens 0-31 on lanes 0-63 and tokens 32-63 on lanes 64-127;
-//   PV  cta_group::2, M = 128, N = 256 twice: CTA c supplies V dims [256c, 256c+256) (16 KB);
-//       T_L holds dims [0,128) / [256,384) on lanes 0-63 / 64-127, T_R [128,256) / [384,512).
-// 36 KB per block per CTA (5 in flight); tensor time per block and SM ~half of the single-CTA
-// kernel's.  Softmax: thread = (row, token half) on SMSP (half, row / 32); the two halves of a
-// row exchange max / sum through SMEM (named barrier per SMSP pair).  Accumulators: thread =
-// (row, dims half of CTA), two warps per SMSP split the 128 columns, 128 fp32 of O each.
-// The leader (rank 0) issues all MMAs; the peer's P' is published to it by a 16-byte bulk
-// copy completing the leader's pp_full (the peer's PV warp forwards it).
-constexpr int k2Slots = 5;
-#ifndef SNAPMLA_2SM_SPF
-#define SNAPMLA_2SM_SPF 0
-#endif
-#ifndef SNAPMLA_2SM_BULK
-#define SNAPMLA_2SM_BULK 1
-#endif
-constexpr bool k2SPrefetch = SNAPMLA_2SM_SPF, k2BulkSignal = SNAPMLA_2SM_BULK;
-constexpr uint32_t k2Stage = 37888;                    // Kq 4 x 4 KB | RoPE 4 KB | V 2 x 8 KB | scales
-constexpr uint32_t k2OffRope = 16384, k2OffV = 20480, k2OffSc = 36864;
-constexpr uint32_t k2Tx = 36864;                       // TMA bytes per block per CTA (scales separate)
-constexpr uint32_t k2OffQr = 0, k2OffP = 8192, k2OffKv = 16384;
-constexpr uint32_t k2OffBar = k2OffKv + k2Slots * k2Stage;
-constexpr uint32_t k2Smem = k2OffBar + 8192 + 1024;
-static_assert(k2Smem <= 232448, "shared memory budget (2-SM kernel)");
-constexpr uint32_t kIdescQk8S = make_idesc(0, 0, 0, 0, 128, 64);
-constexpr uint32_t kIdescQk16S = make_idesc(1, 1, 0, 0, 128, 64);
+// ===================================================================== cta_group::2 helpers
 constexpr uint32_t kIdescPvS = make_idesc(0, 0, 0, 1, 128, 256);
-// TMEM: S slot ss at cols 32 ss; q codes (QK A operand, lanes 0-63) at cols 64-191; T half
-// slot t at cols 192 + 128 t.
-constexpr uint32_t k2TmemQ = 64, k2TmemT = 192;
-
-struct Bars2 {
-  alignas(16) uint8_t sink[kPSlots + 1][16];   // landing bytes of the peer's P' / Q signals (bulk-copy aligned)
-  uint64_t kv_full[k2Slots];    // leader: Kq + RoPE + V of both CTAs (cta_group::2 TMA)
-  uint64_t sc_full[k2Slots];    // local: sigma_K of the block
-  uint64_t kv_empty[k2Slots];   // PV_L + PV_R commits (multicast)
-  uint64_t s_full[kSSlots], s_empty[kSSlots];
-  uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
-  uint64_t t_full[2], t_free[2];
-  uint64_t q_full, q_free;
-  uint32_t tmem_base;
-  float crow[64];
-  float xa[2][64];              // Q-quant prologue: partial amax of each accumulator column group
-  float xm[2][2][64];           // [block parity][token half][row] partial max of t
-  float xl[2][2][64], xw[2][2][64];   // partial l and max of w
-  float stat[kPSlots][3][64];
-};
-static_assert(sizeof(Bars2) <= 8192, "barrier region (2-SM kernel)");
-#define B2(field) (bar0 + (uint32_t)offsetof(Bars2, field))
-
 #define SNAPMLA_QK8S(ta, bo, acc)                                                              \
   "add.u32 t, %1, " #ta ";\n\tadd.s64 b, %2, " #bo ";\n\t"                                     \
   "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [t], b, %3, " acc ";\n\t"
 #define SNAPMLA_QK16S(ao)                                                                      \
   "add.s64 a, %4, " #ao ";\n\tadd.s64 b, %5, " #ao ";\n\t"                                     \
   "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %6, pt;\n\t"
-// K operand boxes are 32 rows x 128 B (4 KB apart): K step kk at (kk / 4) * 4096 + (kk % 4) * 32
-__device__ __forceinline__ void qk_issue_2sm(uint32_t dS, uint32_t tQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
-                                             uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, t;\n\t"
-      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      SNAPMLA_QK8S(0, 0, "pf") SNAPMLA_QK8S(8, 2, "pt") SNAPMLA_QK8S(16, 4, "pt") SNAPMLA_QK8S(24, 6, "pt")
-      SNAPMLA_QK8S(32, 256, "pt") SNAPMLA_QK8S(40, 258, "pt") SNAPMLA_QK8S(48, 260, "pt") SNAPMLA_QK8S(56, 262, "pt")
-      SNAPMLA_QK8S(64, 512, "pt") SNAPMLA_QK8S(72, 514, "pt") SNAPMLA_QK8S(80, 516, "pt") SNAPMLA_QK8S(88, 518, "pt")
-      SNAPMLA_QK8S(96, 768, "pt") SNAPMLA_QK8S(104, 770, "pt") SNAPMLA_QK8S(112, 772, "pt") SNAPMLA_QK8S(120, 774, "pt")
-      SNAPMLA_QK16S(0) SNAPMLA_QK16S(2) SNAPMLA_QK16S(4) SNAPMLA_QK16S(6)
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %8;\n\t}"
-      ::"r"(dS), "r"(tQ), "l"(dK), "r"(kIdescQk8S), "l"(dQr), "l"(dKr), "r"(kIdescQk16S), "r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
 // One PV half (cta_group::2, N = 256 = 128 dims from each CTA): 2 x K = 32; commits multicast
 // to t_full, p_empty and kv_empty of both CTAs.
 __device__ __forceinline__ void pv_issue_2sm(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t, uint32_t bar_p,
@@ -1541,52 +895,155 @@ __device__ __forceinline__ void pv_issue_2sm(uint32_t dT, uint64_t dP, uint64_t 
       : "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    mla_decode_2sm_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv32,
-                          const __grid_constant__ CUtensorMap tm_rope32, const DecodeParams p) {
+// ===================================================================== 2-SM block-pair kernel
+// 64 < rows <= 128 (DeepSeek-R1's 128 heads; LongCat MTP-2).  The two 64-row head tiles of a
+// key range are a CTA pair (cluster of 2) and every contraction is a cta_group::2 MMA at M = 128
+// (64 rows per CTA), processed over PAIRS of key blocks (A, B) = (j, j + 1):
+//   QK  N = 128: CTA 0 supplies block A's 64 tokens, CTA 1 block B's (each the full 576 dims:
+//       4 FP8 boxes X = dims 0-255, Y = dims 256-511, and the RoPE box R).  Each CTA gets S for its
+//       rows with block A on lanes 0-63 and block B on lanes 64-127 (scripts/pair_probe.cu), so a
+//       softmax thread owns a whole row of ONE block: no cross-thread exchange (SMSPs 0-1 run
+//       block A, SMSPs 2-3 block B of the same rows at the same time).
+//   PV  N = 256 per half: CTA 0 supplies V dims 256-511, CTA 1 dims 0-255 of the block, from the
+//       same SMEM offset in both CTAs (the leader's descriptor addresses both): once QK(pair) has
+//       completed, CTA 0 reloads X <- B dims 256-511 and CTA 1 reloads Y <- A dims 0-255
+//       ("phase 2", an L2 hit: the peer loaded those bytes in phase 1); PV(A) then reads Y and
+//       PV(B) reads X in both CTAs.  T lanes 0-63 = dims 256-511, lanes 64-127 = dims 0-255.
+// 40.5 KB per pair per CTA in SMEM (4 pairs = 8 blocks in flight per cluster), DRAM bytes stay
+// algorithmic.  A unit with an odd block count ends in a half pair: block B is absent (no loads,
+// softmax writes m = -inf, the accumulators skip it; the QK / PV MMAs still run on stale SMEM
+// and their outputs are never read).  Cross-CTA signals as in §7.8: the peer's phase-1/2 TMA
+// complete on the leader's kv_full / v_full (cta_group::2 TMA), its S-slot and T-half releases
+// and P' readiness are forwarded to the leader by its idle issue warps.
+constexpr int kBpSlots = 4;
+// 16 warps: 0-7 accumulators (2 per SMSP), 8 TMA, 9 QK, 10 / 11 PV_L / PV_R (peer CTA: 9-11
+// forward its signals), 12-15 softmax.  setmaxnreg only redistributes the CTA's launch
+// allocation (512 x 128), so per SMSP 2 x 176 + 40 + 120 = 512 = 4 x 128.  (A 20-warp layout
+// with two token-half softmax warps per SMSP measured slower: its 480-register budget per SMSP
+// starves the accumulators.)
+constexpr int kBpThreads = 512, kBpWarpTma = 8, kBpWarpQk = 9, kBpWarpPv = 10, kBpWarpSm = 12;
+constexpr uint32_t kBpRegsAcc = 176, kBpRegsSm = 120, kBpRegsIssue = 40;
+static_assert(2 * kBpRegsAcc + kBpRegsSm + kBpRegsIssue <= 4 * 128, "setmaxnreg budget per SMSP (block-pair kernel)");
+constexpr uint32_t kBpStage = 41984;   // X 16 KB | Y 16 KB | RoPE 8 KB | sigma_K of A (256 B) and B (256 B)
+constexpr uint32_t kBpOffX = 0, kBpOffY = 16384, kBpOffR = 32768, kBpOffSc = 40960;
+constexpr uint32_t kBpTx1 = 40960, kBpTx2 = 16384;   // TMA bytes per CTA: phase 1 (own block), phase 2 (V half)
+constexpr uint32_t kBpOffQr = 0, kBpOffP = 8192, kBpOffKv = 8192 + kPSlots * 8192;
+constexpr uint32_t kBpOffBar = kBpOffKv + kBpSlots * kBpStage;
+constexpr uint32_t kBpBarBytes = 8192;
+constexpr uint32_t kBpSmem = kBpOffBar + kBpBarBytes + 1024;
+static_assert(kBpSmem <= 232448, "shared memory budget (block-pair kernel)");
+constexpr uint32_t kIdescQk8P = make_idesc(0, 0, 0, 0, 128, 128);
+constexpr uint32_t kIdescQk16P = make_idesc(1, 1, 0, 0, 128, 128);
+// TMEM: S pair slot ss at cols 64 ss; q codes (QK A operand, both lane halves) at cols 128-255;
+// T half slot h (L = 0, R = 1) at cols 256 + 128 h.
+constexpr uint32_t kBpTmemQ = 128, kBpTmemT = 256;
+
+struct BarsP {
+  alignas(16) uint8_t sink[kPSlots + 1][16];   // landing bytes of the peer's P' / Q signals
+  uint64_t kv_full[kBpSlots];    // leader: phase-1 TMA of both CTAs
+  uint64_t v_full[kBpSlots];     // leader: phase-2 TMA of both CTAs
+  uint64_t sc_full[kBpSlots];    // local: sigma_K of A and B
+  uint64_t qk_done[kBpSlots];    // both: QK(pair) complete (multicast commit) -> phase 2 may overwrite
+  uint64_t kv_empty[kBpSlots];   // both: PV_L(B) + PV_R(B) complete (multicast commits)
+  uint64_t s_full[kSSlots], s_empty[kSSlots];
+  uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
+  uint64_t t_full[2], t_free[2];
+  uint64_t q_full, q_free;
+  uint32_t tmem_base;
+  float crow[64];
+  float xa[2][64];
+  float stat[kPSlots][2][3][64];   // [pair slot][block A / B][m, sigma_p, l][row]
+};
+static_assert(sizeof(BarsP) <= kBpBarBytes, "barrier region (block-pair kernel)");
+#define BP(field) (bar0 + (uint32_t)offsetof(BarsP, field))
+
+// QK of a block pair: 16 x kind::f8f6f4 + 4 x kind::f16, cta_group::2, N = 128; commits
+// multicast to s_full (softmax) and qk_done (phase-2 TMA) of both CTAs.
+__device__ __forceinline__ void qk_issue_bp(uint32_t dS, uint32_t tQ, uint64_t dK, uint64_t dQr, uint64_t dKr,
+                                            uint32_t bar_s, uint32_t bar_q) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, t;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      SNAPMLA_QK8S(0, 0, "pf") SNAPMLA_QK8S(8, 2, "pt") SNAPMLA_QK8S(16, 4, "pt") SNAPMLA_QK8S(24, 6, "pt")
+      SNAPMLA_QK8S(32, 512, "pt") SNAPMLA_QK8S(40, 514, "pt") SNAPMLA_QK8S(48, 516, "pt") SNAPMLA_QK8S(56, 518, "pt")
+      SNAPMLA_QK8S(64, 1024, "pt") SNAPMLA_QK8S(72, 1026, "pt") SNAPMLA_QK8S(80, 1028, "pt") SNAPMLA_QK8S(88, 1030, "pt")
+      SNAPMLA_QK8S(96, 1536, "pt") SNAPMLA_QK8S(104, 1538, "pt") SNAPMLA_QK8S(112, 1540, "pt") SNAPMLA_QK8S(120, 1542, "pt")
+      SNAPMLA_QK16S(0) SNAPMLA_QK16S(2) SNAPMLA_QK16S(4) SNAPMLA_QK16S(6)
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %9;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], %9;\n\t}"
+      ::"r"(dS), "r"(tQ), "l"(dK), "r"(kIdescQk8P), "l"(dQr), "l"(dKr), "r"(kIdescQk16P), "r"(bar_s), "r"(bar_q),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// PV half of block A: 2 x K = 32, commit multicast to t_full only
+__device__ __forceinline__ void pv_issue_bp_a(uint32_t dT, uint64_t dP, uint64_t dV, uint32_t bar_t) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%4], %5;\n\t}"
+      ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPvS), "r"(bar_t), "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
+    mla_decode_bp_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
+                         const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar0 = sbase + k2OffBar;
+  const uint32_t bar0 = sbase + kBpOffBar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < k2Slots; ++i) {
-      mbar_init(B2(kv_full) + 8 * i, 1);
-      mbar_init(B2(sc_full) + 8 * i, 1);
-      mbar_init(B2(kv_empty) + 8 * i, 2);
+    for (int i = 0; i < kBpSlots; ++i) {
+      mbar_init(BP(kv_full) + 8 * i, 1);
+      mbar_init(BP(v_full) + 8 * i, 1);
+      mbar_init(BP(sc_full) + 8 * i, 1);
+      mbar_init(BP(qk_done) + 8 * i, 1);
+      mbar_init(BP(kv_empty) + 8 * i, 2);
     }
     for (int i = 0; i < kSSlots; ++i) {
-      mbar_init(B2(s_full) + 8 * i, 1);
-      mbar_init(B2(s_empty) + 8 * i, leader ? 4 + 1 : 4);   // leader: 4 local warps + the peer's forward; peer: local
+      mbar_init(BP(s_full) + 8 * i, 1);
+      mbar_init(BP(s_empty) + 8 * i, leader ? 4 + 1 : 4);
     }
     for (int i = 0; i < kPSlots; ++i) {
-      mbar_init(B2(p_full) + 8 * i, 4);        // local softmax warps (stats + P')
-      mbar_init(B2(pp_full) + 8 * i, 1);       // leader: the peer's P' (its forwarding warp)
-      mbar_init(B2(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 local accumulator warps
+      mbar_init(BP(p_full) + 8 * i, 4);
+      mbar_init(BP(pp_full) + 8 * i, 1);
+      mbar_init(BP(p_empty) + 8 * i, 2 + 8);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(B2(t_full) + 8 * i, 1);
-      mbar_init(B2(t_free) + 8 * i, leader ? 8 + 1 : 8);   // leader: 8 local warps + the peer's forward; peer: local
+      mbar_init(BP(t_full) + 8 * i, 1);
+      mbar_init(BP(t_free) + 8 * i, leader ? 8 + 1 : 8);
     }
-    mbar_init(B2(q_full), leader ? 12 + 1 : 12);   // 8 acc + 4 softmax local warps (+ the peer's forward)
-    mbar_init(B2(q_free), 1);
+    mbar_init(BP(q_full), leader ? 12 + 1 : 12);
+    mbar_init(BP(q_free), 1);
     fence_barrier_init();
   }
-  if (warp == kWarpTma && lane == 0) {
+  if (warp == kBpWarpTma && lane == 0) {
     tma_prefetch_desc(&tm_kv);
-    tma_prefetch_desc(&tm_kv32);
-    tma_prefetch_desc(&tm_rope32);
+    tma_prefetch_desc(&tm_rope);
   }
-  if (warp == kWarpQk) tmem_alloc_pair(B2(tmem_base), 512);
+  if (warp == kBpWarpQk) tmem_alloc_pair(BP(tmem_base), 512);
   tc_fence_before();
   __syncthreads();
   cluster_sync();
   tc_fence_after();
-  const uint32_t tmem = lds_u32(B2(tmem_base));
+  const uint32_t tmem = lds_u32(BP(tmem_base));
 
   pdl_wait();
+  pdl_launch_dependents();
   const int ht = (int)cta;
   const int g = blockIdx.x / 2;
   const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
@@ -1596,171 +1053,211 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   UnitIter it{p.cum, lo, hi, g, has_work ? __ldg(p.first_req + g) : 0, has_work ? p.batch : 0};
   Unit u;
 
-  if (warp >= kWarpTma && warp < kWarpSoftmax) {
-    regs_dec<kRegsIssue>();
-    if (warp == kWarpTma) {
-      // ============================ TMA producer (both CTAs) ============================
+  if (warp >= kBpWarpTma && warp < kBpWarpSm) {
+    regs_dec<kBpRegsIssue>();
+    if (warp == kBpWarpTma) {
+      // ===================== TMA producer (both CTAs): phase 1 and phase 2 =====================
+      // One thread serves two streams: phase 1 of pair n1 (slot free: kv_empty) and phase 2 of
+      // pair n2 < n1 (QK(n2) complete: qk_done); it polls both so neither waits on the other.
       if (lane == 0) {
-        const uint64_t pol = l2_policy_evict_first();
-        const uint32_t kv_full_leader = mapa_shared(B2(kv_full), 0);
-        uint32_t n = 0;
-        while (it.next(u)) {
-          const int32_t* bt = p.block_table + (int64_t)u.b * p.max_pages;
-          prefetch_block_table(bt, u.k0, u.k1);
-          for (int j = u.k0; j < u.k1; ++j, ++n) {
-            const uint32_t st = n % k2Slots;
-            mbar_wait_backoff(B2(kv_empty) + 8 * st, ((n / k2Slots) & 1) ^ 1);
-            TRACE(TR_TMA, n);
-            const int row = __ldg(bt + j) * kPage;
-            const uint32_t slot = sbase + k2OffKv + st * k2Stage;
-            const uint32_t sc = B2(sc_full) + 8 * st;
-            mbar_arrive_expect_tx(sc, 256);
-            bulk_load(slot + k2OffSc, p.kv_scale + (int64_t)row, 128, sc, pol);
-            bulk_load(slot + k2OffSc + 128, p.kv_scale + (int64_t)row + 32, 128, sc, pol);
-            if (leader) mbar_arrive_expect_tx(B2(kv_full) + 8 * st, 2 * k2Tx);
-            const uint32_t fb = kv_full_leader + 8 * st;
-            const int rq = row + 32 * (int)cta;   // this CTA's token half (QK operand)
+        const uint64_t pol = l2_policy_evict_first(), pol_keep = l2_policy_evict_normal();
+        const uint32_t kv_full_leader = mapa_shared(BP(kv_full), 0), v_full_leader = mapa_shared(BP(v_full), 0);
+        UnitIter it1 = it, it2 = it;
+        Unit u1, u2;
+        bool live1 = it1.next(u1), live2 = it2.next(u2);
+        int j1 = live1 ? u1.k0 : 0, j2 = live2 ? u2.k0 : 0;
+        if (live1) prefetch_block_table(p.block_table + (int64_t)u1.b * p.max_pages, u1.k0, u1.k1);
+        uint32_t n1 = 0, n2 = 0;
+        while (live2) {
+          bool did = false;
+          if (live1 && n1 < n2 + kBpSlots) {
+            const uint32_t st = n1 % kBpSlots;
+            if (mbar_try_wait_ns(BP(kv_empty) + 8 * st, ((n1 / kBpSlots) & 1) ^ 1, n2 < n1 ? 200u : 100000u)) {
+              TRACE(TR_TMA, n1);
+              const int32_t* bt = p.block_table + (int64_t)u1.b * p.max_pages;
+              const bool hasB = j1 + 1 < u1.k1;
+              const int rowA = __ldg(bt + j1) * kPage, rowB = hasB ? __ldg(bt + j1 + 1) * kPage : 0;
+              const uint32_t slot = sbase + kBpOffKv + st * kBpStage;
+              const uint32_t sc = BP(sc_full) + 8 * st;
+              mbar_arrive_expect_tx(sc, hasB ? 512 : 256);
+              bulk_load(slot + kBpOffSc, p.kv_scale + (int64_t)rowA, 256, sc, pol);
+              if (hasB) bulk_load(slot + kBpOffSc + 256, p.kv_scale + (int64_t)rowB, 256, sc, pol);
+              if (leader) mbar_arrive_expect_tx(BP(kv_full) + 8 * st, hasB ? 2 * kBpTx1 : kBpTx1);
+              if (leader || hasB) {
+                const int row = leader ? rowA : rowB;
+                const uint32_t fb = kv_full_leader + 8 * st;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tma_load_2d_cg2(slot + c * 4096, &tm_kv32, fb, c * 128, rq, pol);
-            tma_load_2d_cg2(slot + k2OffRope, &tm_rope32, fb, 0, rq, pol);
-#pragma unroll
-            for (int i = 0; i < 2; ++i)           // this CTA's dims half of V (PV operand)
-              tma_load_2d_cg2(slot + k2OffV + i * kBoxBytes, &tm_kv, fb, (2 * (int)cta + i) * 128, row, pol);
+                for (int c = 0; c < 4; ++c)   // the half the peer reloads in phase 2 stays in L2 (evict_normal)
+                  tma_load_2d_cg2(slot + c * kBoxBytes, &tm_kv, fb, c * 128, row,
+                                  ((c >> 1) == (int)cta) ? pol_keep : pol);
+                tma_load_2d_cg2(slot + kBpOffR, &tm_rope, fb, 0, row, pol);
+              }
+              ++n1;
+              j1 += 2;
+              if (j1 >= u1.k1) {
+                live1 = it1.next(u1);
+                if (live1) {
+                  j1 = u1.k0;
+                  prefetch_block_table(p.block_table + (int64_t)u1.b * p.max_pages, u1.k0, u1.k1);
+                }
+              }
+              did = true;
+            }
+          }
+          if (n2 < n1) {
+            const uint32_t st = n2 % kBpSlots;
+            if (mbar_try_wait_ns(BP(qk_done) + 8 * st, (n2 / kBpSlots) & 1, live1 && n1 < n2 + kBpSlots ? 200u : 100000u)) {
+              const int32_t* bt = p.block_table + (int64_t)u2.b * p.max_pages;
+              const bool hasB = j2 + 1 < u2.k1;
+              const uint32_t slot = sbase + kBpOffKv + st * kBpStage;
+              const uint32_t fb = v_full_leader + 8 * st;
+              if (leader) mbar_arrive_expect_tx(BP(v_full) + 8 * st, hasB ? 2 * kBpTx2 : kBpTx2);
+              if (!leader) {           // CTA 1: Y <- block A dims 0-255
+                const int rowA = __ldg(bt + j2) * kPage;
+                tma_load_2d_cg2(slot + kBpOffY, &tm_kv, fb, 0, rowA, pol);
+                tma_load_2d_cg2(slot + kBpOffY + kBoxBytes, &tm_kv, fb, 128, rowA, pol);
+              } else if (hasB) {       // CTA 0: X <- block B dims 256-511
+                const int rowB = __ldg(bt + j2 + 1) * kPage;
+                tma_load_2d_cg2(slot + kBpOffX, &tm_kv, fb, 256, rowB, pol);
+                tma_load_2d_cg2(slot + kBpOffX + kBoxBytes, &tm_kv, fb, 384, rowB, pol);
+              }
+              ++n2;
+              j2 += 2;
+              if (j2 >= u2.k1) {
+                live2 = it2.next(u2);
+                if (live2) j2 = u2.k0;
+              }
+              did = true;
+            }
           }
         }
       }
-    } else if (warp == kWarpQk && leader) {
+    } else if (warp == kBpWarpQk && leader) {
       // ================================ QK issuer (leader) ================================
-      {
-        const uint64_t dQr = make_smem_desc(sbase + k2OffQr, 16, 1024, LAYOUT_SW128);
-        uint32_t n = 0, unit = 0;
-        while (it.next(u)) {
-          mbar_wait(B2(q_full), unit & 1, 2, unit);
-          for (int j = u.k0; j < u.k1; ++j, ++n) {
-            const uint32_t st = n % k2Slots, ss = n % kSSlots;
-            mbar_wait(B2(kv_full) + 8 * st, (n / k2Slots) & 1, 3, n);
-            if (lane == 0) TRACE(TR_S2, n);
-            mbar_wait(B2(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
-            tc_fence_after();
-            if (lane == 0) TRACE(TR_QK, n);
-            const uint32_t kv = sbase + k2OffKv + st * k2Stage;
-            qk_issue_2sm(tmem + 32 * ss, tmem + k2TmemQ, make_smem_desc(kv, 16, 1024, LAYOUT_SW128), dQr,
-                         make_smem_desc(kv + k2OffRope, 16, 1024, LAYOUT_SW128), B2(s_full) + 8 * ss);
-          }
-          mma_commit_pair_ws(B2(q_free));
-          ++unit;
+      const uint64_t dQr = make_smem_desc(sbase + kBpOffQr, 16, 1024, LAYOUT_SW128);
+      uint32_t n = 0, unit = 0;
+      while (it.next(u)) {
+        mbar_wait(BP(q_full), unit & 1, 2, unit);
+        for (int j = u.k0; j < u.k1; j += 2, ++n) {
+          const uint32_t st = n % kBpSlots, ss = n % kSSlots;
+          mbar_wait(BP(kv_full) + 8 * st, (n / kBpSlots) & 1, 3, n);
+          if (lane == 0) TRACE(TR_C1, n);
+          mbar_wait(BP(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
+          tc_fence_after();
+          if (lane == 0) TRACE(TR_QK, n);
+          const uint32_t kv = sbase + kBpOffKv + st * kBpStage;
+          qk_issue_bp(tmem + 64 * ss, tmem + kBpTmemQ, make_smem_desc(kv + kBpOffX, 16, 1024, LAYOUT_SW128), dQr,
+                      make_smem_desc(kv + kBpOffR, 16, 1024, LAYOUT_SW128), BP(s_full) + 8 * ss,
+                      BP(qk_done) + 8 * st);
         }
+        mma_commit_pair_ws(BP(q_free));
+        ++unit;
       }
     } else if (leader) {
       // ============================ PV_L / PV_R issuers (leader) ============================
-      const uint32_t half = warp - kWarpPv;
+      const uint32_t half = warp - kBpWarpPv;
+      const uint32_t dT = tmem + kBpTmemT + 128 * half;
       uint32_t n = 0;
       while (it.next(u)) {
-        for (int j = u.k0; j < u.k1; ++j, ++n) {
-          const uint32_t st = n % k2Slots, ps = n % kPSlots;
-          const uint32_t h = 2 * n + half, ts = h % 2;
-          mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
-          mbar_wait(B2(pp_full) + 8 * ps, (n / kPSlots) & 1, 14, n);
+        for (int j = u.k0; j < u.k1; j += 2, ++n) {
+          const uint32_t st = n % kBpSlots, ps = n % kPSlots;
+          mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
+          mbar_wait(BP(pp_full) + 8 * ps, (n / kPSlots) & 1, 14, n);
           if (lane == 0 && half == 0) TRACE(TR_S5, n);
-          if (h >= 2) mbar_wait(B2(t_free) + 8 * ts, (h / 2 - 1) & 1, 6, n);
-          tc_fence_after();
-          if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
-          const uint32_t pA = sbase + k2OffP + ps * 4096;
-          const uint32_t vb = sbase + k2OffKv + st * k2Stage + k2OffV + half * kBoxBytes;
-          pv_issue_2sm(tmem + k2TmemT + 128 * ts, make_smem_desc(pA, 1024, 128, LAYOUT_NONE),
-                       make_smem_desc(vb, kBoxBytes, 1024, LAYOUT_SW128), B2(t_full) + 8 * ts, B2(p_empty) + 8 * ps,
-                       B2(kv_empty) + 8 * st);
+          mbar_wait(BP(v_full) + 8 * st, (n / kBpSlots) & 1, 13, n);
+          if (lane == 0 && half == 0) TRACE(TR_C2, n);
+          const uint32_t kv = sbase + kBpOffKv + st * kBpStage;
+          const uint32_t pA = sbase + kBpOffP + ps * 8192;
+#pragma unroll
+          for (int blk = 0; blk < 2; ++blk) {
+            const uint32_t nb = 2 * n + blk;
+            if (nb >= 1) mbar_wait(BP(t_free) + 8 * half, (nb - 1) & 1, 6, n);
+            tc_fence_after();
+            if (lane == 0 && blk == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+            const uint64_t dP = make_smem_desc(pA + 4096 * blk, 1024, 128, LAYOUT_NONE);
+            const uint64_t dV = make_smem_desc(kv + (blk ? kBpOffX : kBpOffY) + half * kBoxBytes, kBoxBytes, 1024,
+                                               LAYOUT_SW128);
+            if (blk == 0)
+              pv_issue_bp_a(dT, dP, dV, BP(t_full) + 8 * half);
+            else
+              pv_issue_2sm(dT, dP, dV, BP(t_full) + 8 * half, BP(p_empty) + 8 * ps, BP(kv_empty) + 8 * st);
+          }
         }
       }
-    } else if (warp == kWarpQk) {
-      // ======== peer: forward "S slot read" (its 4 softmax warps, local barrier) to the leader ========
-      // (remote arrives issued by the compute warps themselves stall them; measured)
-      const uint32_t s_empty_leader = mapa_shared(B2(s_empty), 0);
-      const uint32_t q_full_leader = mapa_shared(B2(q_full), 0);
+    } else if (warp == kBpWarpQk) {
+      // ======== peer: forward its Q readiness and "S slot read" to the leader ========
+      const uint32_t s_empty_leader = mapa_shared(BP(s_empty), 0);
+      const uint32_t q_full_leader = mapa_shared(BP(q_full), 0);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        // this CTA's Q (codes in TMEM, q_r' in SMEM) -> the leader's QK: 16-byte bulk copy
-        // completing the leader's q_full after the local q_full (acquire) of all 12 writers
-        mbar_wait(B2(q_full), unit & 1, 18, unit);
+        mbar_wait(BP(q_full), unit & 1, 18, unit);
         tc_fence_after();
-        if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(B2(sink), 0) + 16 * kPSlots, sbase + k2OffQr);
+        if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(BP(sink), 0) + 16 * kPSlots, sbase + kBpOffQr);
         __syncwarp();
         ++unit;
-        for (int j = u.k0; j < u.k1; ++j, ++n) {
+        for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t ss = n % kSSlots;
-          mbar_wait(B2(s_empty) + 8 * ss, (n / kSSlots) & 1, 16, n);
+          mbar_wait(BP(s_empty) + 8 * ss, (n / kSSlots) & 1, 16, n);
           if (lane == 0) mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
           __syncwarp();
         }
       }
-    } else if (warp == kWarpPv + 1) {
-      // ======== peer: forward "T half read" (its 8 accumulator warps, local barrier) to the leader ========
-      const uint32_t t_free_leader = mapa_shared(B2(t_free), 0);
-      uint32_t n = 0;
+    } else if (warp == kBpWarpPv + 1) {
+      // ======== peer: forward "T half read" (its 8 accumulator warps) to the leader ========
+      const uint32_t t_free_leader = mapa_shared(BP(t_free), 0);
+      uint32_t nb = 0;
       while (it.next(u)) {
-        for (int j = u.k0; j < u.k1; ++j, ++n) {
+        for (int j = u.k0; j < u.k1; j += 2) {
 #pragma unroll 1
-          for (int hf = 0; hf < 2; ++hf) {
-            mbar_wait(B2(t_free) + 8 * hf, n & 1, 17, n);
-            if (lane == 0) mbar_arrive_cluster_relaxed(t_free_leader + 8 * hf);
-            __syncwarp();
+          for (int blk = 0; blk < 2; ++blk, ++nb) {
+#pragma unroll 1
+            for (int hf = 0; hf < 2; ++hf) {
+              mbar_wait(BP(t_free) + 8 * hf, nb & 1, 17, nb);
+              if (lane == 0) mbar_arrive_cluster_relaxed(t_free_leader + 8 * hf);
+              __syncwarp();
+            }
           }
         }
       }
-    } else if (warp == kWarpPv) {
-      // ============ peer: forward "P' written" to the leader's PV issue (relaxed arrive) ============
-      // A release arrive on the remote barrier from the softmax warps themselves stalls them
-      // (~1-2K cycles, measured); this warp observes the local p_full (acquire: the softmax
-      // warps' SMEM writes and proxy fences precede it) and signals the leader.
-      const uint32_t pp_leader = mapa_shared(B2(pp_full), 0);
+    } else if (warp == kBpWarpPv) {
+      // ======== peer: forward "P' written" to the leader's PV issue (16-byte bulk-copy signal) ========
+      const uint32_t pp_leader = mapa_shared(BP(pp_full), 0);
       uint32_t n = 0;
       while (it.next(u)) {
-        for (int j = u.k0; j < u.k1; ++j, ++n) {
+        for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t ps = n % kPSlots;
-          mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 15, n);
-          if (lane == 0) {
-            if constexpr (k2BulkSignal)
-              mbar_signal_peer_tx(pp_leader + 8 * ps, mapa_shared(B2(sink), 0) + 16 * ps, sbase + k2OffP + ps * 4096);
-            else
-              mbar_arrive_cluster_relaxed(pp_leader + 8 * ps);
-          }
+          mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 15, n);
+          if (lane == 0)
+            mbar_signal_peer_tx(pp_leader + 8 * ps, mapa_shared(BP(sink), 0) + 16 * ps, sbase + kBpOffP + ps * 8192);
           __syncwarp();
         }
       }
     }
-  } else if (warp >= kWarpSoftmax) {
-    if constexpr (kRegsSoftmax > 128) regs_inc<kRegsSoftmax>();
-    else regs_dec<kRegsSoftmax>();
-    const int k = warp & 3;                  // SMSP: row group k & 1, token half k >> 1
-    const int hk = k >> 1;
+  } else if (warp >= kBpWarpSm) {
+    regs_dec<kBpRegsSm>();
+    // ======== softmax / scale fusion / P quantization: thread = (row, block of the pair) ========
+    const int k = warp & 3;                  // SMSP = TMEM lane quarter
+    const int hk = k >> 1;                   // block of the pair: 0 = A (lanes 0-63), 1 = B (lanes 64-127)
     const int r = 32 * (k & 1) + lane;       // row inside the head tile
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    const uint32_t pair_bar = 2 + (k & 1);   // named barrier of the SMSP pair (k, k ^ 2)
-    const uint32_t s_empty_leader = mapa_shared(B2(s_empty), 0);
-    const uint32_t q_full_leader = mapa_shared(B2(q_full), 0);
     uint32_t n = 0, unit = 0;
     while (it.next(u)) {
-      // ---------------- Fused-Q-Quant prologue (a2).  The 2-SM QK reads its TMEM A operand
-      // per N half: rows for the CTA-0 token half from lanes 0-63, for the CTA-1 half from
-      // lanes 64-127 (measured: scripts/exp/dbg_2sm_s.py), so every warp writes the codes
-      // of its 32 rows into its own lane quarter; SMSPs 0-1 also write q_r' and c.
-      // The 512 q codes of a row are computed by the two accumulator warps of the row's SMSP
-      // (256 each, written into that SMSP's TMEM lane quarter); the softmax warp combines their
-      // partial amax into sigma_q and writes q_r' / sigma_q and c (SMSPs 0-1).
+      // ---------------- Fused-Q-Quant prologue (a2): as in the 2-SM kernel (codes by the
+      // accumulator warps into every lane quarter; q_r' / sigma_q and c by SMSPs 0-1)
       if (unit > 0) {
-        mbar_wait(B2(q_free), (unit - 1) & 1, 11, unit);
+        mbar_wait(BP(q_free), (unit - 1) & 1, 11, unit);
         named_bar_sync(1, 128);
       }
-      named_bar_sync(4, 384);   // partial amax of the accumulator warps written
+      named_bar_sync(4, 384);
       {
-        const float amax = fmaxf(lds_f32(B2(xa) + 4 * r), lds_f32(B2(xa) + 256 + 4 * r));
+        const float amax = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
         if (hk == 0) {
           const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-          sts_f32(B2(crow) + 4 * r, sq * p.scale_log2);
+          sts_f32(BP(crow) + 4 * r, sq * p.scale_log2);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
@@ -1773,148 +1270,156 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                                      __float2bfloat16_rn(div_by(f.y, sq, rsq)));
               wd[e] = *reinterpret_cast<uint32_t*>(&o2);
             }
-            sts_u4(sbase + k2OffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+            sts_u4(sbase + kBpOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
           }
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(q_full));   // local (the peer's warp 9 forwards it)
+        if (lane == 0) mbar_arrive(BP(q_full));
       }
       named_bar_sync(1, 128);
-      const float c_row = lds_f32(B2(crow) + 4 * r);
+      const float c_row = lds_f32(BP(crow) + 4 * r);
       const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
-      // One exchange per block between the two token halves of a row: each half exponentiates
-      // against its OWN max m_h; then (m_h, l_h, max_h w) are exchanged and half h rescales by
-      // f_h = 2^{(m_h - m) c}: l = sum_h f_h l_h, M_b = max_h f_h max_h(w), P' = E4M3(w f_h 448 / M_b)
-      // (P' depends only on w / max_block(w)).  S(n+1) is loaded from TMEM before
-      // block n's P' / stats stores.
-      float tt[32];
-      for (int j = u.k0; j < u.k1; ++j, ++n) {
-        const uint32_t st = n % k2Slots, ss = n % kSSlots, ps = n % kPSlots, par = n & 1;
-        if (j == u.k0 || !k2SPrefetch) {
-          mbar_wait(B2(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
+      float tt[64];
+      for (int j = u.k0; j < u.k1; j += 2, ++n) {
+        const uint32_t st = n % kBpSlots, ss = n % kSSlots, ps = n % kPSlots;
+        const int blk = j + hk;
+        const bool valid = blk < u.k1;
+        if (j == u.k0) {   // first pair of the unit; later pairs were prefetched (below)
+          mbar_wait(BP(s_full) + 8 * ss, (n / kSSlots) & 1, 7, n);
           tc_fence_after();
-          tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss, *reinterpret_cast<uint32_t(*)[32]>(tt));
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss + 32, *reinterpret_cast<uint32_t(*)[32]>(tt + 32));
         }
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_IN, n);
         tmem_wait_ld();
+        if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_SM_IN, n);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(s_empty) + 8 * ss);   // peer: forwarded by its warp 9
-        mbar_wait(B2(sc_full) + 8 * st, (n / k2Slots) & 1, 12, n);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S1, n);
-        const uint32_t sk = sbase + k2OffKv + st * k2Stage + k2OffSc + 128 * hk;
-        float4 skv[8];
+        if (lane == 0) mbar_arrive(BP(s_empty) + 8 * ss);   // peer: forwarded by its warp 9
+        float st_m = -INFINITY, st_sig = 1.f, lsum = 0.f;
+        uint32_t pw[16];
+        if (valid) {
+          mbar_wait(BP(sc_full) + 8 * st, (n / kBpSlots) & 1, 12, n);
+          if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_S1, n);
+          // sigma_K of the block, 16 tokens per batch of loads: the four loads of a batch issue
+          // back to back (one exposed shared-load latency per batch, ~16 extra registers live)
+          const uint32_t sk = sbase + kBpOffKv + st * kBpStage + kBpOffSc + 256 * hk;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) skv[e] = lds_f4(sk + 16 * e);
+          for (int e0 = 0; e0 < 64; e0 += 16) {                           // step 3 (descale)
+            float4 s4[4];
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 s4 = skv[e / 4];
-          const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4.x, s4.y));
-          const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4.z, s4.w));
-          tt[e] = a.x;
-          tt[e + 1] = a.y;
-          tt[e + 2] = b.x;
-          tt[e + 3] = b.y;
+            for (int i = 0; i < 4; ++i) s4[i] = lds_f4(sk + 4 * (e0 + 4 * i));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int e = e0 + 4 * i;
+              const float2 a = __fmul2_rn(make_float2(tt[e], tt[e + 1]), make_float2(s4[i].x, s4[i].y));
+              const float2 b = __fmul2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(s4[i].z, s4[i].w));
+              tt[e] = a.x;
+              tt[e + 1] = a.y;
+              tt[e + 2] = b.x;
+              tt[e + 3] = b.y;
+            }
+          }
+          const int nvalid = L - blk * kBc;
+          if (nvalid < 64) {                                              // ragged tail (R19)
+#pragma unroll
+            for (int e = 0; e < 64; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
+          }
+          float m0 = fmax3(tt[0], tt[1], tt[2]), m1 = fmax3(tt[3], tt[4], tt[5]);
+          float m2 = fmax3(tt[6], tt[7], tt[8]), m3 = fmax3(tt[9], tt[10], tt[11]);
+#pragma unroll
+          for (int e = 12; e < 60; e += 8) {
+            m0 = fmax3(m0, tt[e], tt[e + 1]);
+            m1 = fmax3(m1, tt[e + 2], tt[e + 3]);
+            m2 = fmax3(m2, tt[e + 4], tt[e + 5]);
+            m3 = fmax3(m3, tt[e + 6], tt[e + 7]);
+          }
+          const float mx = fmax3(fmax3(m0, m1, m2), fmax3(m3, tt[60], tt[61]), fmaxf(tt[62], tt[63]));
+          const float mc = mx == -INFINITY ? 0.f : mx * c_row;
+          if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_S2, n);
+          float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+          float mb0 = 0.f, mb1 = 0.f;
+          float4 s4b[4];
+#pragma unroll
+          for (int e = 0; e < 64; e += 4) {
+            if ((e & 15) == 0) {   // next batch of 16 sigma_K
+#pragma unroll
+              for (int i = 0; i < 4; ++i) s4b[i] = lds_f4(sk + 4 * (e + 4 * i));
+            }
+            const float4 s4 = s4b[(e & 15) / 4];
+            const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+            const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mc, -mc));
+#ifdef SNAPMLA_SOL_NOEXP   // speed-of-light experiment only (wrong results): MUFU-free softmax
+            const float2 p0 = __fmul2_rn(e0, make_float2(0.5f, 0.5f)), p1 = __fmul2_rn(e1, make_float2(0.5f, 0.5f));
+#else
+            const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));   // step 5
+            const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
+#endif
+            ls0 = __fadd2_rn(ls0, p0);
+            ls1 = __fadd2_rn(ls1, p1);
+            const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));   // step 6: w = p sigma_K
+            const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
+            tt[e] = w0.x;
+            tt[e + 1] = w0.y;
+            tt[e + 2] = w1.x;
+            tt[e + 3] = w1.y;
+            mb0 = fmax3(mb0, w0.x, w0.y);
+            mb1 = fmax3(mb1, w1.x, w1.y);
+          }
+          lsum = (ls0.x + ls0.y) + (ls1.x + ls1.y);
+          const float mb = fmaxf(mb0, mb1);
+          if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_S3, n);
+          // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block is skipped (R11)
+          st_m = mb > 0.f ? mc : -INFINITY;
+          st_sig = mb * (1.0f / 448.0f);   // sigma_p = M_b / 448 (one rounding; not bit-gated)
+          const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
+          const float2 inv2 = make_float2(inv, inv);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
+            const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
+            pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
+          }
         }
-        const int nvalid = L - (j * kBc + 32 * hk);
-        if (nvalid < 32) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) tt[e] = e < nvalid ? tt[e] : -INFINITY;
-        }
-        float mx0 = fmaxf(fmaxf(tt[0], tt[1]), tt[2]), mx1 = fmaxf(fmaxf(tt[3], tt[4]), tt[5]);
-#pragma unroll
-        for (int e = 6; e < 30; e += 4) {
-          mx0 = fmaxf(fmaxf(mx0, tt[e]), tt[e + 1]);
-          mx1 = fmaxf(fmaxf(mx1, tt[e + 2]), tt[e + 3]);
-        }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(tt[30], tt[31]));   // this half's max of t
-        const float mch = mx == -INFINITY ? 0.f : mx * c_row;
-        float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
-        float mb0 = 0.f, mb1 = 0.f;
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 s4 = skv[e / 4];
-          const float2 e0 = __ffma2_rn(make_float2(tt[e], tt[e + 1]), make_float2(c_row, c_row), make_float2(-mch, -mch));
-          const float2 e1 = __ffma2_rn(make_float2(tt[e + 2], tt[e + 3]), make_float2(c_row, c_row), make_float2(-mch, -mch));
-          const float2 p0 = make_float2(ex2_approx(e0.x), ex2_approx(e0.y));
-          const float2 p1 = make_float2(ex2_approx(e1.x), ex2_approx(e1.y));
-          const float2 w0 = __fmul2_rn(p0, make_float2(s4.x, s4.y));
-          const float2 w1 = __fmul2_rn(p1, make_float2(s4.z, s4.w));
-          ls0 = __fadd2_rn(ls0, p0);
-          ls1 = __fadd2_rn(ls1, p1);
-          tt[e] = w0.x;
-          tt[e + 1] = w0.y;
-          tt[e + 2] = w1.x;
-          tt[e + 3] = w1.y;
-          mb0 = fmaxf(fmaxf(mb0, w0.x), w0.y);
-          mb1 = fmaxf(fmaxf(mb1, w1.x), w1.y);
-        }
-        const float lsh = (ls0.x + ls0.y) + (ls1.x + ls1.y);
-        const float mbh = fmaxf(mb0, mb1);
-        const uint32_t xo = 4 * ((par * 2 + hk) * 64 + r), xp = 4 * ((par * 2 + (hk ^ 1)) * 64 + r);
-        sts_f32(B2(xm) + xo, mx);
-        sts_f32(B2(xl) + xo, lsh);
-        sts_f32(B2(xw) + xo, mbh);
-        named_bar_sync(pair_bar, 64);
-        const float mxo = lds_f32(B2(xm) + xp), lso = lds_f32(B2(xl) + xp), mbo = lds_f32(B2(xw) + xp);
-        const float mtot = fmaxf(mx, mxo);
-        const float mc = mtot == -INFINITY ? 0.f : mtot * c_row;
-        const float fme = mx == -INFINITY ? 0.f : ex2_approx(mch - mc);          // f_h of this half
-        const float fot = mxo == -INFINITY ? 0.f : ex2_approx(mxo * c_row - mc); // f_h of the other half
-        const float lsum = lsh * fme + lso * fot;
-        const float mb = fmaxf(mbh * fme, mbo * fot);
-        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = __fdiv_rn(mb, 448.0f);
-        const float inv = mb > 0.f ? __fdividef(448.0f, mb) * fme : 0.f;
-        const float2 inv2 = make_float2(inv, inv);
-        uint32_t pw[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float2 a = __fmul2_rn(make_float2(tt[4 * e], tt[4 * e + 1]), inv2);
-          const float2 b = __fmul2_rn(make_float2(tt[4 * e + 2], tt[4 * e + 3]), inv2);
-          pw[e] = cvt4_e4m3(a.x, a.y, b.x, b.y);
-        }
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S3, n);
-        if (k2SPrefetch && j + 1 < u.k1) {   // prefetch S(n+1)
+        if (j + 2 < u.k1) {   // prefetch S(n+1): its TMEM load overlaps this pair's P' / stats stores
           const uint32_t ss1 = (n + 1) % kSSlots;
-          mbar_wait(B2(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
+          mbar_wait(BP(s_full) + 8 * ss1, ((n + 1) / kSSlots) & 1, 7, n + 1);
           tc_fence_after();
-          tmem_ld_32x32b_x32(tmem + lane_base + 32 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
+          tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss1 + 32, *reinterpret_cast<uint32_t(*)[32]>(tt + 32));
         }
-        mbar_wait(B2(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_S4, n);
-        if (hk == 0) {
-          const uint32_t sa = B2(stat) + ps * (3 * 64 * 4) + 4 * r;
+        mbar_wait(BP(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
+        if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_S4, n);
+        {
+          const uint32_t sa = BP(stat) + ((ps * 2 + hk) * 3 * 64 + r) * 4;
           sts_f32(sa, st_m);
           sts_f32(sa + 256, st_sig);
           sts_f32(sa + 512, lsum);
         }
-        const uint32_t pdst = sbase + k2OffP + ps * 4096 + r * 16;
-        sts_u4(pdst + (2 * hk) * 1024, pw[0], pw[1], pw[2], pw[3]);
-        sts_u4(pdst + (2 * hk + 1) * 1024, pw[4], pw[5], pw[6], pw[7]);
+        if (valid) {   // K-major core matrices: byte(row, tok) = (tok / 16) * 1024 + row * 16 + tok % 16
+          const uint32_t pdst = sbase + kBpOffP + ps * 8192 + hk * 4096 + r * 16;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sts_u4(pdst + c * 1024, pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+        }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(p_full) + 8 * ps);   // local: P' + stats written
-        if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
+        if (lane == 0) mbar_arrive(BP(p_full) + 8 * ps);
+        if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_SM_OUT, n);
       }
       ++unit;
     }
   } else {
-    if constexpr (kRegsAcc > 128) regs_inc<kRegsAcc>();
-    else regs_dec<kRegsAcc>();
-    // ========= accumulators: thread = (row, CTA dims half), two warps per SMSP split columns =========
+    regs_inc<kBpRegsAcc>();
+    // ========= accumulators: thread = (row, CTA dims half of T), two warps per SMSP split columns =========
     const int k = warp & 3, cg = warp >> 2;
     const int r = 32 * (k & 1) + lane;
     const int head = ht * kHeadTile + r;
     const bool row_ok = head < p.num_heads;
     const uint32_t lane_base = (uint32_t)(32 * k) << 16;
-    const int dbase = (k >> 1) * 256 + 64 * cg;   // T_L column c -> dim dbase + c; T_R -> + 128
-    const uint32_t stat0 = B2(stat) + 4 * r;
-    const uint32_t t_free_leader = mapa_shared(B2(t_free), 0);
+    const int dbase = (k < 2 ? 256 : 0) + 64 * cg;   // lanes 0-63: CTA 0's V columns = dims 256-511
     uint32_t n = 0, unit = 0;
     while (it.next(u)) {
-      // ---- Q-quant prologue share: codes [256 cg, 256 cg + 256) of row r into this SMSP's lanes
-      if (unit > 0) mbar_wait(B2(q_free), (unit - 1) & 1, 19, unit);
+      if (unit > 0) mbar_wait(BP(q_free), (unit - 1) & 1, 19, unit);
       {
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk) + 32 * cg;
         float amax = 0.f;
@@ -1933,13 +1438,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        sts_f32(B2(xa) + 256 * cg + 4 * r, amax);
+        sts_f32(BP(xa) + 256 * cg + 4 * r, amax);
         named_bar_sync(4, 384);
-        const float am = fmaxf(lds_f32(B2(xa) + 4 * r), lds_f32(B2(xa) + 256 + 4 * r));
+        const float am = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
         const float sq = fmaxf(__fdiv_rn(am, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
 #pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {   // 128 codes = 32 TMEM columns per store
+        for (int ci = 0; ci < 2; ++ci) {
           uint32_t qa[32];
 #pragma unroll
           for (int g8 = 0; g8 < 8; ++g8) {
@@ -1954,74 +1459,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
             }
           }
-          tmem_st_32x32b_x32(tmem + lane_base + k2TmemQ + 32 * (2 * cg + ci), qa);
+          tmem_st_32x32b_x32(tmem + lane_base + kBpTmemQ + 32 * (2 * cg + ci), qa);
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(q_full));
+        if (lane == 0) mbar_arrive(BP(q_full));
       }
       ++unit;
-      const uint32_t n0 = n;
       float o[128];
 #pragma unroll
       for (int e = 0; e < 128; ++e) o[e] = 0.f;
       float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
-      for (int j = u.k0; j < u.k1; ++j, ++n) {
+      for (int j = u.k0; j < u.k1; j += 2, ++n) {
         const uint32_t ps = n % kPSlots;
-        mbar_wait(B2(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
         if (threadIdx.x == 0) TRACE(TR_C0, n);
-        const uint32_t sa = stat0 + ps * (3 * 64 * 4);
-        const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
+        const uint32_t sa = BP(stat) + (ps * 2 * 3 * 64 + r) * 4;
+        const float mbA = lds_f32(sa), sbA = lds_f32(sa + 256), lbA = lds_f32(sa + 512);
+        const float mbB = lds_f32(sa + 768), sbB = lds_f32(sa + 1024), lbB = lds_f32(sa + 1280);
         __syncwarp();
-        if (lane == 0) mbar_arrive(B2(p_empty) + 8 * ps);
-        const float m_new = fmaxf(m_ref, mb);
-        const bool first = n == n0;
-        const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
-        float gamma = 0.f;
-        if (first) {
-          m_O = mb;
-          sig_O = sb;
-          l_run = lb;
-          m_ref = mb;
-        } else if (!skip) {
-          gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);
-          l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
-          m_ref = m_new;
-          m_O = mb;
-          sig_O = sb;
-        }
-        const float2 g2 = make_float2(gamma, gamma);
+        if (lane == 0) mbar_arrive(BP(p_empty) + 8 * ps);
+#pragma unroll 1
+        for (int blk = 0; blk < 2; ++blk) {
+          const uint32_t nb = 2 * n + blk;
+          const float mb = blk ? mbB : mbA, sb = blk ? sbB : sbA, lb = blk ? lbB : lbA;
+          const float m_new = fmaxf(m_ref, mb);
+          const bool first = j == u.k0 && blk == 0;
+#ifdef SNAPMLA_SOL_NOACC   // speed-of-light experiment only (wrong results): no accumulate FMAs
+          const bool skip = true;
+#else
+          const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
+#endif
+          float gamma = 0.f;
+          if (first) {
+            m_O = mb;
+            sig_O = sb;
+            l_run = lb;
+            m_ref = mb;
+          } else if (!skip) {
+            gamma = ex2_approx(m_O - mb) * __fdividef(sig_O, sb);
+            l_run = l_run * ex2_approx(m_ref - m_new) + lb * ex2_approx(mb - m_new);
+            m_ref = m_new;
+            m_O = mb;
+            sig_O = sb;
+          }
+          const float2 g2 = make_float2(gamma, gamma);
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const uint32_t h = 2 * n + hf, ts = h % 2;
-          mbar_wait(B2(t_full) + 8 * ts, (h / 2) & 1, 10, n);
-          tc_fence_after();
-          const uint32_t taddr = tmem + lane_base + k2TmemT + 128 * ts + 64 * cg;
-          uint32_t tv[2][16];
-          tmem_ld_32x32b_x16(taddr, tv[0]);
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait(BP(t_full) + 8 * hf, nb & 1, 10, nb);
+            tc_fence_after();
+            const uint32_t taddr = tmem + lane_base + kBpTmemT + 128 * hf + 64 * cg;
+            uint32_t tv[2][16];   // T in 16-column chunks, software-pipelined
+            tmem_ld_32x32b_x16(taddr, tv[0]);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            tmem_wait_ld();
-            if (c < 3) tmem_ld_32x32b_x16(taddr + 16 * (c + 1), tv[(c + 1) & 1]);
-            else {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(B2(t_free) + 8 * ts);   // peer: forwarded by its warp 11
-            }
-            const uint32_t* cur = tv[c & 1];
-            if (!skip) {
+            for (int c = 0; c < 4; ++c) {
+              tmem_wait_ld();
+              if (c < 3) tmem_ld_32x32b_x16(taddr + 16 * (c + 1), tv[(c + 1) & 1]);
+              else {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(BP(t_free) + 8 * hf);   // peer: forwarded by its warp 11
+              }
+              const uint32_t* cur = tv[c & 1];
+              if (!skip) {
 #pragma unroll
-              for (int e = 0; e < 16; e += 2) {
-                const int oi = 64 * hf + 16 * c + e;
-                const float2 a = __ffma2_rn(make_float2(o[oi], o[oi + 1]), g2,
-                                            make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
-                o[oi] = a.x;
-                o[oi + 1] = a.y;
+                for (int e = 0; e < 16; e += 2) {
+                  const int oi = 64 * hf + 16 * c + e;
+                  const float2 a = __ffma2_rn(make_float2(o[oi], o[oi + 1]), g2,
+                                              make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])));
+                  o[oi] = a.x;
+                  o[oi + 1] = a.y;
+                }
               }
             }
+            if (threadIdx.x == 0 && blk == 0) TRACE(hf == 0 ? TR_C_L : TR_C_R, n);
           }
-          if (threadIdx.x == 0) TRACE(hf == 0 ? TR_C_L : TR_C_R, n);
         }
       }
       const float f = l_run > 0.f ? sig_O * ex2_approx(m_O - m_ref) / l_run : 0.f;
@@ -2044,7 +1557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync();
-  if (warp == kWarpQk) {
+  if (warp == kBpWarpQk) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, 512);
   }
@@ -2081,15 +1594,80 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static unsigned long long* g_trace = nullptr;
-static int g_pair = 0;   // kernel for 64 < rows <= 128: 0 = single-CTA (default), 2 = 2-SM (§7.8), 1 = CTA pair (§7.6)
-static int g_pair_groups = 0, g_pair_max_clusters = -1;   // debug: force the single-CTA kernel for 64 < rows <= 128
+// ---- process-wide host state (thread-safe): the debug switches below, a per-device
+// record of one-time launch attributes, and a small cache of encoded tensor maps keyed by
+// (device, pool base, rows, kind).  Nothing else is global.
+static std::atomic<unsigned long long*> g_trace{nullptr};
+static std::atomic<int> g_kernel{-1};   // 64 < rows <= 128: -1 auto, 0 single-CTA, 1 block-pair (debug override)
+
+struct DeviceInfo {
+  int sms = 0;
+  bool attr_done[3] = {false, false, false};   // MaxDynamicSharedMemorySize set: FP8, BF16, block-pair
+  int bp_max_clusters = -1;
+};
+constexpr int kMaxDevices = 64;
+static std::mutex g_host_mu;
+static DeviceInfo g_dev[kMaxDevices];
+
+struct TmapEntry {
+  int dev;
+  const void* base;
+  uint64_t rows;
+  int kind;   // 0 FP8 content, 1 BF16 content (baseline), 2 RoPE
+  CUtensorMap map;
+};
+constexpr int kTmapCache = 32;
+static TmapEntry g_tmap[kTmapCache];
+static int g_tmap_n = 0, g_tmap_next = 0;
+
+static int current_device() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kMaxDevices ? dev : -1;
+}
 
 int device_num_sms() {
-  int dev = 0, n = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  return n;
+  const int dev = current_device();
+  if (dev < 0) return 0;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (g_dev[dev].sms == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    g_dev[dev].sms = n;
+  }
+  return g_dev[dev].sms;
+}
+
+// the encoded map for (current device, base, rows, kind), encoding it on first use
+static bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap* out) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  for (int i = 0; i < g_tmap_n; ++i) {
+    const TmapEntry& e = g_tmap[i];
+    if (e.dev == dev && e.base == base && e.rows == rows && e.kind == kind) {
+      *out = e.map;
+      return true;
+    }
+  }
+  CUtensorMap m;
+  const bool ok = kind == 0   ? encode_2d(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, kDc, rows, kDc, 128, 64)
+                  : kind == 1 ? encode_2d(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, kDc, rows, kDc * 2, 64, 64)
+                              : encode_2d(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, kDr, rows, kDr * 2, 64, 64);
+  if (!ok) return false;
+  TmapEntry& e = g_tmap[g_tmap_next];
+  e = TmapEntry{dev, base, rows, kind, m};
+  g_tmap_next = (g_tmap_next + 1) % kTmapCache;
+  if (g_tmap_n < kTmapCache) ++g_tmap_n;
+  *out = m;
+  return true;
+}
+
+// one-time per device: dynamic SMEM attribute of a kernel (and the block-pair cluster occupancy)
+template <typename K>
+static bool ensure_attr(int dev, int which, K kernel, uint32_t smem) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (g_dev[dev].attr_done[which]) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+  g_dev[dev].attr_done[which] = true;
+  return true;
 }
 
 }  // namespace snapmla
@@ -2097,23 +1675,21 @@ int device_num_sms() {
 using namespace snapmla;
 
 // Debug only (include/snapmla_debug.h): subsequent decodes record a CTA-0 event timeline.
-extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
-// Kernel for 64 < rows <= 128: 0 = the single-CTA kernel (default; two CTAs per key range, each
-// with its own M = 64 QK and PV), 2 = 2-SM kernel, 1 = CTA-pair kernel (both experimental).
-extern "C" void mla_debug_set_pair(int v) { g_pair = v; }
-// Debug only: cap the number of CTA pairs of the pair kernel (0 = all that fit); returns the
-// occupancy limit cudaOccupancyMaxActiveClusters reported on the last pair launch (-1: none yet).
-extern "C" int mla_debug_set_pair_groups(int v) {
-  g_pair_groups = v;
-  return g_pair_max_clusters;
-}
-
+extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace.store(dev_buf); }
+// Debug / test only: force the kernel for 64 < rows <= 128 (-1 = automatic, the default).
+extern "C" void mla_debug_set_pair(int v) { g_kernel.store(v); }
 extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms) {
   if (batch < 0 || num_heads <= 0) return 0;
   if (num_sms <= 0) num_sms = device_num_sms();
   if (num_sms <= 0) num_sms = 148;
   return ws_layout(batch, num_heads, num_sms).total;
 }
+
+// The block-pair kernel wins once each cluster streams enough pairs to amortise its longer
+// start-up; the host cannot read seq_lens (device-resident), so it decides on the block
+// table's extent, an upper bound of the work (scripts/cmp_kernels.py: crossover between
+// 8K and 16K blocks on the DeepSeek-R1 shape).
+constexpr int64_t kBpMinBlocks = 16384;
 
 static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, const void* kv_rope,
                                 const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
@@ -2132,59 +1708,38 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   if (!aligned(q, 16) || !aligned(kv_fp8, 128) || !aligned(kv_rope, 128) || (!bf16 && !aligned(kv_scale, 16)) ||
       !aligned(workspace, 256))
     return MLA_ERR_ALIGN;
+  if (num_pages == 0) return MLA_ERR_SHAPE;
+  const int dev = current_device();
   const int sms = device_num_sms();
-  if (sms <= 0) return MLA_ERR_CUDA;
+  if (dev < 0 || sms <= 0) return MLA_ERR_CUDA;
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   if (workspace_bytes < wl.total) return MLA_ERR_WORKSPACE;
   const int n_ht = (num_heads + kHeadTile - 1) / kHeadTile;
-  const bool pair = !bf16 && n_ht == 2 && g_pair == 1;
-  const bool two_sm = !bf16 && n_ht == 2 && g_pair == 2;   // 64 < rows <= 128: CTA-pair kernel (experimental, off by default)
+  const int force = g_kernel.load();
+  const bool bp = !bf16 && n_ht == 2 &&
+                  (force == 1 || (force < 0 && (int64_t)batch * max_pages_per_seq >= kBpMinBlocks));
   int groups = sms / n_ht;
-  if (two_sm) {
-    static int max_clusters2 = -1;
-    if (max_clusters2 < 0) {
-      if (cudaFuncSetAttribute(mla_decode_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem) !=
-          cudaSuccess)
-        return MLA_ERR_CUDA;
+  if (bp) {
+    if (!ensure_attr(dev, 2, mla_decode_bp_kernel, kBpSmem)) return MLA_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    if (g_dev[dev].bp_max_clusters < 0) {
       cudaLaunchConfig_t oc = {};
       oc.gridDim = dim3(2 * groups);
-      oc.blockDim = dim3(kThreads);
-      oc.dynamicSmemBytes = k2Smem;
+      oc.blockDim = dim3(kBpThreads);
+      oc.dynamicSmemBytes = kBpSmem;
       int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, mla_decode_2sm_kernel, &oc) != cudaSuccess) return MLA_ERR_CUDA;
-      max_clusters2 = nc;
+      if (cudaOccupancyMaxActiveClusters(&nc, mla_decode_bp_kernel, &oc) != cudaSuccess) return MLA_ERR_CUDA;
+      g_dev[dev].bp_max_clusters = nc;
     }
-    if (max_clusters2 > 0 && max_clusters2 < groups) groups = max_clusters2;
+    const int nc = g_dev[dev].bp_max_clusters;
+    if (nc > 0 && nc < groups) groups = nc;
+  } else if (!(bf16 ? ensure_attr(dev, 1, mla_decode_kernel<true>, Variant<true>::kSmem)
+                    : ensure_attr(dev, 0, mla_decode_kernel<false>, Variant<false>::kSmem))) {
+    return MLA_ERR_CUDA;
   }
-  if (pair) {
-    static int max_clusters = -1;
-    if (max_clusters < 0) {
-      if (cudaFuncSetAttribute(mla_decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemBytes) !=
-          cudaSuccess)
-        return MLA_ERR_CUDA;
-      cudaLaunchConfig_t oc = {};
-      oc.gridDim = dim3(2 * groups);
-      oc.blockDim = dim3(kThreads);
-      oc.dynamicSmemBytes = kPSmemBytes;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, mla_decode_pair_kernel, &oc) != cudaSuccess) return MLA_ERR_CUDA;
-      max_clusters = nc;
-    }
-    g_pair_max_clusters = max_clusters;
-    if (max_clusters > 0 && max_clusters < groups) groups = max_clusters;
-    if (g_pair_groups > 0 && g_pair_groups < groups) groups = g_pair_groups;
-  }
-
-  CUtensorMap tm_kv, tm_rope, tm_kv32, tm_rope32;
+  CUtensorMap tm_kv, tm_rope;
   const uint64_t rows = (uint64_t)num_pages * kPage;
-  if (num_pages == 0) return MLA_ERR_SHAPE;
-  if (bf16 ? !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_fp8, kDc, rows, kDc * 2, 64, 64)
-           : !encode_2d(&tm_kv, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 64))
-    return MLA_ERR_CUDA;
-  if (!encode_2d(&tm_rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_rope, kDr, rows, kDr * 2, 64, 64))
-    return MLA_ERR_CUDA;
-  if (two_sm && (!encode_2d(&tm_kv32, CU_TENSOR_MAP_DATA_TYPE_UINT8, kv_fp8, kDc, rows, kDc, 128, 32) ||
-                 !encode_2d(&tm_rope32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kv_rope, kDr, rows, kDr * 2, 64, 32)))
+  if (!cached_tmap(dev, kv_fp8, rows, bf16 ? 1 : 0, &tm_kv) || !cached_tmap(dev, kv_rope, rows, 2, &tm_rope))
     return MLA_ERR_CUDA;
 
   char* ws = static_cast<char*>(workspace);
@@ -2192,13 +1747,21 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   int32_t* cum = reinterpret_cast<int32_t*>(ws + wl.cum);
   int32_t* first = reinterpret_cast<int32_t*>(ws + wl.first);
   cudaStream_t st = (cudaStream_t)stream;
-  plan_kernel<<<1, 1024, 0, st>>>(seq_lens, batch, num_heads, groups, hdr, cum, first);
-  if (cudaGetLastError() != cudaSuccess) return MLA_ERR_CUDA;
+  cudaLaunchAttribute pdl_attr[1];
+  pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+  {
+    cudaLaunchConfig_t pc = {};
+    pc.gridDim = dim3(1);
+    pc.blockDim = dim3(1024);
+    pc.stream = st;
+    pc.attrs = pdl_attr;
+    pc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&pc, plan_kernel, seq_lens, batch, num_heads, groups, hdr, cum, first, sms) != cudaSuccess)
+      return MLA_ERR_CUDA;
+  }
 
-  const uint32_t smem = two_sm ? k2Smem : pair ? kPSmemBytes : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
-  if (!pair && !two_sm && cudaFuncSetAttribute(bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return MLA_ERR_CUDA;
+  const uint32_t smem = bp ? kBpSmem : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
   DecodeParams prm;
   prm.q = (const __nv_bfloat16*)q;
   prm.kv_fp8 = static_cast<const uint8_t*>(kv_fp8);
@@ -2218,13 +1781,13 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   prm.heads = heads;
   prm.max_pages = max_pages_per_seq;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
-  prm.trace = g_trace;
+  prm.trace = g_trace.load();
   // programmatic dependent launch: the decode CTAs start (barrier init, TMEM
   // alloc, descriptor prefetch) while the plan kernel runs; griddepcontrol.wait
   // in the kernel orders every read of the plan / cache after it.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(groups * n_ht);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(bp ? kBpThreads : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -2232,11 +1795,8 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (two_sm) {
-    if (cudaLaunchKernelEx(&cfg, mla_decode_2sm_kernel, tm_kv, tm_kv32, tm_rope32, prm) != cudaSuccess)
-      return MLA_ERR_CUDA;
-  } else if (pair) {
-    if (cudaLaunchKernelEx(&cfg, mla_decode_pair_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
+  if (bp) {
+    if (cudaLaunchKernelEx(&cfg, mla_decode_bp_kernel, tm_kv, tm_rope, prm) != cudaSuccess) return MLA_ERR_CUDA;
   } else if (cudaLaunchKernelEx(&cfg, bf16 ? mla_decode_kernel<true> : mla_decode_kernel<false>, tm_kv, tm_rope,
                                 prm) != cudaSuccess) {
     return MLA_ERR_CUDA;

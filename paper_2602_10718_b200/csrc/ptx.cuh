@@ -106,6 +106,31 @@ DEVI void mbar_wait(uint32_t a, uint32_t parity, int = -1, int = -1) {
 DEVI void mbar_wait_backoff(uint32_t a, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) __nanosleep(SNAPMLA_BACKOFF_NS);
 }
+// probe with a hardware suspend of up to `ns` (a producer serving two barrier streams
+// alternates between them without spinning)
+DEVI bool mbar_try_wait_ns(uint32_t addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+// non-blocking probe
+DEVI bool mbar_test_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
 // ------------------------------------------------------------- clusters
 DEVI uint32_t cluster_ctarank() {
@@ -514,6 +539,12 @@ DEVI float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// three-input max (FMNMX3 on sm_100)
+DEVI float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
 DEVI float lg2_approx(float x) {
   float y;

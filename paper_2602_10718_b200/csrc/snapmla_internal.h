@@ -26,7 +26,7 @@ inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_
 // float lse_part[slots*n_ht*64] | float o_part[slots*n_ht*64*512]
 // slot of (request b, group g) = b + g; slots = batch + groups.
 constexpr int kHdr = 16;
-enum HdrField { H_TOTAL = 0, H_PER = 1, H_GROUPS = 2, H_NHT = 3, H_BATCH = 4, H_HEADS = 5 };
+enum HdrField { H_TOTAL = 0, H_PER = 1, H_GROUPS = 2, H_NHT = 3, H_BATCH = 4, H_HEADS = 5, H_SMS = 6 };
 
 struct WsLayout {
   size_t cum, first, lse, o, total;

@@ -59,10 +59,6 @@ def lib():
     L.mla_kv_append_bf16.argtypes = [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _P, _P, _P]
     L.mla_decode_bf16.restype = _I
     L.mla_decode_bf16.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
-    if os.environ.get("SNAPMLA_PAIR"):   # kernel choice for 64 < rows <= 128 (include/snapmla_debug.h)
-        L.mla_debug_set_pair(int(os.environ["SNAPMLA_PAIR"]))
-    if os.environ.get("SNAPMLA_PAIR_GROUPS"):
-        L.mla_debug_set_pair_groups(int(os.environ["SNAPMLA_PAIR_GROUPS"]))
     _lib = L
     return L
 

@@ -1,5 +1,7 @@
-"""CTA-0 (leader) event timeline of the 2-SM kernel (SNAPMLA_TRACE build), DS-R1 shape.
-   SNAPMLA_LIB=paper_2602_10718_b200/libsnapmla_trace.so python scripts/trace_2sm.py"""
+"""CTA-0 (leader) event timeline of the block-pair 2-SM kernel (SNAPMLA_TRACE build), DS-R1 shape.
+   SNAPMLA_LIB=paper_2602_10718_b200/libsnapmla_trace.so python scripts/trace_bp.py [B H L]
+Events are indexed by the CTA's n-th block PAIR; prints the median per-pair period and the
+median gap between consecutive stages of one pair."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
@@ -20,7 +22,7 @@ for s in range(0, B * L, 1 << 18):
 q = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
 sl = torch.full((B,), L, dtype=torch.int32, device=dev)
 lib = ops.lib()
-lib.mla_debug_set_pair(int(os.environ.get("V", "2")))
+lib.mla_debug_set_pair(int(os.environ.get("V", "1")))
 tr = torch.zeros(16 * 256 + 2 * 1024, dtype=torch.int64, device=dev)
 lib.mla_debug_set_trace.argtypes = [ctypes.c_void_p]
 for i in range(3):
@@ -30,23 +32,23 @@ for i in range(3):
 torch.cuda.synchronize()
 lib.mla_debug_set_trace(None)
 t = tr.cpu().numpy()[:16 * 256].reshape(16, 256).astype(np.int64)
-names = ["TMA", "QK", "PV_L", "PV_R", "SM_in", "SM_out", "C_L", "C_R", "SMsc", "QKkvq", "SMsoft", "SMpemp", "PVpp", "C0", "C1", "C2"]
-nv = int((t[1] > 0).sum())
-def per(e):
-    return np.median(np.diff(t[e][20:min(nv, 200)]))
-print("blocks", nv, "periods:", {names[e]: per(e) for e in (0, 1, 2, 4, 5, 6)})
-def med(a, b):
-    return np.median((t[b] - t[a])[20:min(nv, 200)])
-print("QKkvq-TMA", med(0, 9), "QK-QKkvq", med(9, 1), "SM_in-QK", med(1, 4), "SMsc-SM_in", med(4, 8),
-      "SMsoft-SMsc", med(8, 10), "SMpemp-SMsoft", med(10, 11), "SM_out-SMpemp", med(11, 5),
-      "PVpp-SM_out", med(5, 12), "PV_L-PVpp", med(12, 2), "C0-SM_out", med(5, 13), "C_L-PV_L", med(2, 6), "C_R-C_L", med(6, 7))
-
+N = dict(TMA=0, QK=1, PVL=2, PVR=3, SM_in=4, SM_out=5, C_L=6, C_R=7, S1=8, S2=9, S3=10, S4=11, S5=12, C0=13, C1=14, C2=15)
+nv = int((t[N["QK"]] > 0).sum())
+lo, hi = 10, min(nv, 200)
+print("pairs", nv)
+print("period (median diff):", {k: int(np.median(np.diff(t[v][lo:hi]))) for k, v in N.items() if (t[v][lo:hi] > 0).all()})
+chain = ["TMA", "C1", "QK", "SM_in", "S1", "S2", "S3", "S4", "SM_out", "S5", "C2", "PVL", "C_L", "C_R"]
+print("stage gaps (median over pairs):")
+for a, b in zip(chain[:-1], chain[1:]):
+    d = (t[N[b]] - t[N[a]])[lo:hi]
+    print(f"  {a:>6} -> {b:<6} {int(np.median(d)):8d}")
+print("  SM_out -> C0", int(np.median((t[N["C0"]] - t[N["SM_out"]])[lo:hi])))
 ct = tr.cpu().numpy()[16 * 256:].reshape(-1, 2).astype(np.int64)
 ok = ct[:, 0] > 0
 if ok.any():
     d = (ct[ok, 1] - ct[ok, 0]) / 1e3
     print("CTA durations us: min/median/max", d.min(), np.median(d), d.max(), "span", (ct[ok, 1].max() - ct[ok, 0].min()) / 1e3)
-rel = t - t[0][0]
-print("first blocks (TMA, QK, PV_L, SM_in, SM_out, C_L):")
+rel = t - t[N["TMA"]][0]
+print("first pairs (TMA, QK, SM_in, SM_out, PVL, C_L):")
 for n in range(min(nv, 6)):
-    print(n, [int(rel[e][n]) for e in (0, 1, 2, 4, 5, 6)])
+    print(n, [int(rel[N[e]][n]) for e in ("TMA", "QK", "SM_in", "SM_out", "PVL", "C_L")])

@@ -42,6 +42,26 @@ def test_every_declared_symbol_is_exported(L):
     assert sorted(ops.exported_symbols()) == _declared()
 
 
+def test_debug_header_symbols_exported(L):
+    """include/snapmla_debug.h (trace, kernel override, read-stream measurement) is exported too."""
+    from paper_2602_10718_b200 import ops
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "snapmla_debug.h")).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(mla_[a-z0-9_]+)\s*\(", src)))
+    assert names == ["mla_debug_set_pair", "mla_debug_set_trace", "mla_measure_read_stream"]
+    out = subprocess.run(["nm", "-D", "--defined-only", ops.LIB_PATH], capture_output=True, text=True).stdout
+    for name in names:
+        assert re.search(r"\bT " + name + r"\b", out), name
+
+
+def test_read_stream_argument_checks(L):
+    f = L.mla_measure_read_stream
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    assert f(None, 1024, 4096, 16, None) == 1                 # NULL buffer
+    assert f(4096, 1000, 4096, 16, None) == 2                 # bytes not a multiple of 16
+    assert f(4104, 1024, 4096, 16, None) == 4                 # misaligned buffer
+
+
 def test_sass_is_sm100a_tcgen05_tma(L):
     from paper_2602_10718_b200 import ops
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", ops.LIB_PATH], capture_output=True,

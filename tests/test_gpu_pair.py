@@ -1,6 +1,6 @@
-"""The three kernels for 64 < rows <= 128 (include/snapmla_debug.h mla_debug_set_pair):
-the default single-CTA kernel, the experimental 2-SM (§7.8) and CTA-pair
-(§7.6) kernels, each through the same cases.  Same O7
+"""Both kernels for 64 < rows <= 128, forced through include/snapmla_debug.h
+mla_debug_set_pair: the single-CTA kernel and the block-pair 2-SM kernel
+(§7.9, the default from 16K blocks of work), each through the same cases.  Same O7
 gate as test_gpu_decode.py; the pair kernel must also agree bit for bit with itself
 across runs.  The switch is process-global, so every test restores the default."""
 import numpy as np
@@ -14,13 +14,13 @@ from test_gpu_mtp import _check_mtp
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["single", "pair", "2sm"])
+@pytest.fixture(params=[0, 1], ids=["single", "bp"])
 def pair_kernel(request):
-    """0: single-CTA kernel (§7.3, default), 1: CTA-pair kernel, 2: 2-SM kernel (§7.8)."""
+    """0: single-CTA kernel (§7.3), 1: block-pair 2-SM kernel (§7.9); -1 (automatic) restored after."""
     L = ops.lib()
     L.mla_debug_set_pair(request.param)
     yield request.param
-    L.mla_debug_set_pair(0)
+    L.mla_debug_set_pair(-1)
 
 
 # unit shapes: single blocks (per = 1), odd units (pair + lone block: [148*64+3, 5]),
