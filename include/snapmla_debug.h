@@ -24,6 +24,11 @@ void mla_debug_set_pair(int v);
  * the caller).  Enqueued on `stream`; returns an mla_status. */
 int mla_measure_read_stream(const void* buf, size_t bytes, unsigned long long* sink, int sink_len,
                             void* stream);
+/* Test only: out[i] (device, count bytes, 4-byte aligned, count % 4 == 0) = the E4M3 code the
+ * kernels' encoder (cvt.rn.satfinite.e4m3x2.f32, 4 values per call as the kernels pack them)
+ * gives the fp32 whose bit pattern is first_bits + i.  Used for the exhaustive sweep of all
+ * finite fp32 against oracle.codec.encode_e4m3 (scripts/cvt_sweep.py). */
+int mla_debug_cvt_e4m3(unsigned int first_bits, unsigned int count, unsigned char* out, void* stream);
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,21 @@ enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, T
   } while (0)
 #endif
 
+// Warp-level arrive on a barrier that publishes (or releases) this warp's SMEM writes (reads):
+// by default lane 0 arrives after __syncwarp (one arrival per warp); a SNAPMLA_LANE_ARRIVE build
+// (compute-sanitizer racecheck runs, scripts/sanitize_all.sh) makes every lane arrive, which the
+// tool models as synchronisation; counts scale by kArriveMul.
+#ifdef SNAPMLA_LANE_ARRIVE
+constexpr uint32_t kArriveMul = 32;
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int) { mbar_arrive(bar); }
+#else
+constexpr uint32_t kArriveMul = 1;
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
+}
+#endif
+
 struct Bars {
   uint64_t kv_full[5], kv_empty[5];             // TMA -> QK / PV_L + PV_R -> TMA (max over variants)
   uint64_t s_full[kSSlots], s_empty[kSSlots];   // QK -> softmax / softmax -> QK
@@ -392,8 +407,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(BAR(kv_empty) + 8 * i, 2);
     }
     for (int i = 0; i < kPSlots; ++i) {
-      mbar_init(BAR(p_full) + 8 * i, 4);
-      mbar_init(BAR(p_empty) + 8 * i, 2 + 8);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
+      mbar_init(BAR(p_full) + 8 * i, 4 * kArriveMul);
+      mbar_init(BAR(p_empty) + 8 * i, 2 + 8 * kArriveMul);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(BAR(s_full) + 8 * i, 1);
@@ -751,8 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_C2, n);
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(p_full) + 8 * ps);
+        warp_arrive(BAR(p_full) + 8 * ps, lane);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
       ++unit;
@@ -783,8 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
         const uint32_t sa = stat0 + ps * (3 * 64 * 4);
         const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(p_empty) + 8 * ps);             // stats of this slot consumed
+        warp_arrive(BAR(p_empty) + 8 * ps, lane);                      // stats of this slot consumed
         const float m_new = fmaxf(m_ref, mb);                          // step 4 (running max)
         // a block whose contributions are < 2^-64 of the running total is dropped
         // (Alg.1 loses it to fp32 underflow of exp(s - m)); so is a zero-max block
@@ -949,6 +962,7 @@ struct BarsP {
   uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
   uint64_t t_full[2], t_free[2];
   uint64_t q_full, q_free;
+  uint64_t xa_full;                // Q-quant prologue: the 8 accumulator warps' partial amax written
   uint32_t tmem_base;
   float crow[64];
   float xa[2][64];
@@ -1019,9 +1033,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       mbar_init(BP(s_empty) + 8 * i, leader ? 4 + 1 : 4);
     }
     for (int i = 0; i < kPSlots; ++i) {
-      mbar_init(BP(p_full) + 8 * i, 4);
+      mbar_init(BP(p_full) + 8 * i, 4 * kArriveMul);
       mbar_init(BP(pp_full) + 8 * i, 1);
-      mbar_init(BP(p_empty) + 8 * i, 2 + 8);
+      mbar_init(BP(p_empty) + 8 * i, 2 + 8 * kArriveMul);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(BP(t_full) + 8 * i, 1);
@@ -1029,6 +1043,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     }
     mbar_init(BP(q_full), leader ? 12 + 1 : 12);
     mbar_init(BP(q_free), 1);
+    mbar_init(BP(xa_full), 8 * kArriveMul);
     fence_barrier_init();
   }
   if (warp == kBpWarpTma && lane == 0) {
@@ -1250,7 +1265,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
         mbar_wait(BP(q_free), (unit - 1) & 1, 11, unit);
         named_bar_sync(1, 128);
       }
-      named_bar_sync(4, 384);
+      mbar_wait(BP(xa_full), unit & 1, 20, unit);   // the accumulator warps' partial amax
       {
         const float amax = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
@@ -1402,8 +1417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
           for (int c = 0; c < 4; ++c) sts_u4(pdst + c * 1024, pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
         }
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BP(p_full) + 8 * ps);
+        warp_arrive(BP(p_full) + 8 * ps, lane);
         if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_SM_OUT, n);
       }
       ++unit;
@@ -1439,7 +1453,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
           }
         }
         sts_f32(BP(xa) + 256 * cg + 4 * r, amax);
-        named_bar_sync(4, 384);
+        warp_arrive(BP(xa_full), lane);
+        mbar_wait(BP(xa_full), unit & 1, 21, unit);
         const float am = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
         const float sq = fmaxf(__fdiv_rn(am, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
@@ -1478,8 +1493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
         const uint32_t sa = BP(stat) + (ps * 2 * 3 * 64 + r) * 4;
         const float mbA = lds_f32(sa), sbA = lds_f32(sa + 256), lbA = lds_f32(sa + 512);
         const float mbB = lds_f32(sa + 768), sbB = lds_f32(sa + 1024), lbB = lds_f32(sa + 1280);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BP(p_empty) + 8 * ps);
+        warp_arrive(BP(p_empty) + 8 * ps, lane);
 #pragma unroll 1
         for (int blk = 0; blk < 2; ++blk) {
           const uint32_t nb = 2 * n + blk;

@@ -31,9 +31,32 @@ __global__ void __launch_bounds__(512) read_stream_kernel(const uint4* __restric
   if ((threadIdx.x & 31) == 0) atomicXor(sink + blockIdx.x, (unsigned long long)acc);
 }
 
+// Exhaustive check of the product's E4M3 encoder (cvt4_e4m3 -> cvt.rn.satfinite.e4m3x2.f32, used
+// by the append, the Q quantization and the P quantization): out[i] = E4M3 code of the fp32 whose
+// bit pattern is first + i.  Four consecutive patterns per thread, exactly as the kernels pack them.
+__global__ void __launch_bounds__(256) cvt_sweep_kernel(uint32_t first, uint32_t count, uint32_t* __restrict__ out) {
+  const uint32_t n4 = count / 4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const uint32_t b = first + 4 * i;
+    out[i] = cvt4_e4m3(__uint_as_float(b), __uint_as_float(b + 1), __uint_as_float(b + 2), __uint_as_float(b + 3));
+  }
+}
+
 }  // namespace snapmla
 
 using namespace snapmla;
+
+// Debug / test only (include/snapmla_debug.h).
+extern "C" mla_status mla_debug_cvt_e4m3(uint32_t first_bits, uint32_t count, uint8_t* out, mla_stream_t stream) {
+  if (!out) return MLA_ERR_NULL;
+  if (count % 4 != 0) return MLA_ERR_SHAPE;
+  if (!aligned(out, 4)) return MLA_ERR_ALIGN;
+  if (count == 0) return MLA_OK;
+  const int sms = device_num_sms();
+  if (sms <= 0) return MLA_ERR_CUDA;
+  cvt_sweep_kernel<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(first_bits, count, reinterpret_cast<uint32_t*>(out));
+  return cudaGetLastError() == cudaSuccess ? MLA_OK : MLA_ERR_CUDA;
+}
 
 // Debug / measurement only (include/snapmla_debug.h).
 extern "C" mla_status mla_measure_read_stream(const void* buf, size_t bytes, unsigned long long* sink,
