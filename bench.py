@@ -58,6 +58,8 @@ def parse():
                          "GLOBAL batch split over the ranks (dist.dp_range); auto = strong for longcat (BASELINE "
                          "configs[3]), weak otherwise")
     ap.add_argument("--no-peaks", action="store_true", help="skip the on-box FP8 GEMM / read-stream peak measurement")
+    ap.add_argument("--mx", action="store_true",
+                    help="NEXT-4(b): the MX-scaled P variant (mla_decode_fp8_mx; not the paper's method)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "single", "bp"],
                     help="64 < rows <= 128: force the single-CTA or the block-pair kernel (experiments; "
                          "default: the library's automatic choice)")
@@ -430,6 +432,8 @@ def run_ours(args, rank, world, local_rank):
     def decode(qx):
         if args.bf16:
             ops.mla_decode_bf16(qx, cache.kv_c, cache.kv_rope, block_table, seq_lens, scale, ws)
+        elif args.mx:
+            ops.mla_decode_fp8_mx(qx, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
         else:
             decode_fp8(qx, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, scale, ws)
     gathered, peer_ptrs, sym = None, None, None
@@ -658,10 +662,13 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": scaling_mode(args),
         "vs_baseline": None,
-        "dtype": "bf16 (NEXT-2 unquantized baseline; f32 accumulate)" if args.bf16 else "fp8e4m3 (f32 accumulate; bf16 RoPE)",
+        "dtype": "bf16 (NEXT-2 unquantized baseline; f32 accumulate)" if args.bf16 else
+                 "fp8e4m3, MX power-of-two P scales (NEXT-4(b) variant; f32 accumulate in TMEM; bf16 RoPE)" if args.mx else
+                 "fp8e4m3 (f32 accumulate; bf16 RoPE)",
         "data": "synthetic (seeded MLA-like latent / RoPE distributions, random page permutation)",
         "config": {
-            "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else ""), "global_batch": B_global,
+            "workload": w["name"] + (" [BF16 baseline cache, NEXT-2]" if args.bf16 else
+                                     " [MX-scaled P variant, NEXT-4(b)]" if args.mx else ""), "global_batch": B_global,
             "batch_per_rank": B, "heads": H, "heads_per_rank": heads_local,
             "context": L, "page": 64, "kv_lora_rank": 512, "rope_dim": 64, "mtp": T,
             "parallelism": f"dp{n_dp}tp{tp_world}" + ("+fused-gather" if peer_ptrs is not None else ""),
@@ -669,7 +676,8 @@ def run_ours(args, rank, world, local_rank):
             "l2": f"inputs larger than L2: KV {kv_bytes / 1e9:.2f} GB per rank vs 126 MB L2",
         },
         "roofline": roofline_record(dec_bytes, flops, dec_ms, peaks, args.bf16,
-                                    ("mla_decode_bf16" if args.bf16 else "mla_decode_fp8") + " (plan + decode launches)",
+                                    ("mla_decode_bf16" if args.bf16 else "mla_decode_fp8_mx" if args.mx else
+                                     "mla_decode_fp8") + " (plan + decode launches)",
                                     dec_stats, args.workload, T)
         | {"bytes_per_unit": f"{bytes_per_token} B per cached token + 1152 B per (request, query token, head) q row"},
         "ms_per_step_stats": step_stats,

@@ -153,6 +153,22 @@ mla_status mla_decode_fp8_ex(const void* q, const uint8_t* kv_fp8, const void* k
                              mla_stream_t stream);
 
 /*
+ * mla_decode_fp8_mx -- NEXT-4(b): the MX-scaled P variant (NOT the paper's method; reading R28,
+ * DESIGN.md §7.10).  Same arguments, workspace and follow-up (mla_combine / _f32, num_heads =
+ * q_len x heads rows) as mla_decode_fp8_ex, with q_len x num_heads <= 128.  P' of each 64-token
+ * block is quantized with a power-of-two scale 2^ceil(log2(max w / 448)) instead of max w / 448
+ * (P:696), the exponentials against an integer reference per block, so the tensor core applies
+ * every block's scale (kind::mxf8f6f4.block_scale) and the output accumulates in tensor memory
+ * without per-block rescaling.  Matches oracle.snapmla.decode_mx.  Valid while |logit| x log2(e)
+ * < ~90 (scale exponents are clamped beyond).
+ */
+mla_status mla_decode_fp8_mx(const void* q, const uint8_t* kv_fp8, const void* kv_rope, const float* kv_scale,
+                             const int32_t* block_table, const int32_t* seq_lens, int batch, int num_heads,
+                             int q_len, int kv_lora_rank, int rope_dim, int page_size, int max_pages_per_seq,
+                             int64_t num_pages, float softmax_scale, void* workspace, size_t workspace_bytes,
+                             mla_stream_t stream);
+
+/*
  * mla_combine -- merge split-KV partials left in `workspace` by the preceding
  * mla_decode_fp8 (same batch / num_heads, stream-ordered):
  *   L = log sum_s e^{L_s};   o = sum_s e^{L_s - L} o_s

@@ -208,6 +208,48 @@ def decode_o7(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale,
     return num / den[:, None], m + np.log(den)
 
 
+def decode_mx(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale, block=B_C, p_quant=True):
+    """NEXT-4(b) MX variant as the B200 kernel mla_decode_fp8_mx defines it (NOT the paper's
+    method; DESIGN.md §7.10 and reading R28).  Per row r and 64-token block b (aligned to token 0):
+
+      L2[r,j]  = s[r,j] * log2(e)                               (s: the O7 logits)
+      R[r,b]   = ceil(max_{j in b} L2[r,j])                     integer reference of the block
+      p[r,j]   = 2^(L2[r,j] - R[r,b]) ;  w = p * sigma_K[j]     (scale fusion as in P:237-239)
+      e[r,b]   = ceil(log2(fp32(max_{j in b} w / 448)))         power-of-two P scale (UE8M0)
+      P'[r,j]  = E4M3(fp32(w[r,j] / 2^e[r,b]))
+      num[r,:] = sum_b 2^(e + R) sum_{j in b} dec(P'[r,j]) dec(kc[j,:])
+      den[r]   = sum_b 2^R sum_{j in b} p[r,j] = sum_j 2^L2[r,j] = sum_j exp(s[r,j])
+      o = num / den ;  lse = ln(den)
+
+    The codes do not depend on the integer references (scaling w by 2^k scales 2^e by 2^k),
+    so the kernel's clamped references give the same P'.  ``p_quant=False`` replaces the
+    E4M3 rounding by the identity: then o == O6 exactly (the 2^(e+R) factors cancel).
+    Returns (o [H,512] fp64, lse [H] fp64)."""
+    L = kc.shape[0]
+    s = logits(qc, sq, qr_bits, kc, sk, kr_bits, softmax_scale)
+    L2 = s / np.log(2.0)
+    skd = np.asarray(sk, dtype=np.float64)
+    kd = decode_e4m3(kc)
+    num = np.zeros((s.shape[0], kd.shape[1]))
+    den = np.zeros(s.shape[0])
+    for start in range(0, L, block):
+        sl = slice(start, min(start + block, L))
+        R = np.ceil(L2[:, sl].max(axis=1))
+        p = np.exp2(L2[:, sl] - R[:, None])
+        w = p * skd[None, sl]
+        M = w.max(axis=1)
+        Mf = (M / E4M3_MAX).astype(np.float32).astype(np.float64)
+        e = np.ceil(np.log2(np.where(Mf > 0, Mf, 1.0)))
+        if p_quant:
+            A = decode_e4m3(encode_e4m3((w / np.exp2(e)[:, None]).astype(np.float32)))
+            A[M == 0] = 0.0
+        else:
+            A = w / np.exp2(e)[:, None]
+        num += np.exp2(e + R)[:, None] * (A @ kd[sl])
+        den += np.exp2(R) * p.sum(axis=1)
+    return num / den[:, None], np.log(den)
+
+
 # --------------------------------------------------------------------------
 # Algorithm 1, transcribed literally (dual warp group, o^L / o^R halves)
 # --------------------------------------------------------------------------
@@ -338,11 +380,13 @@ def combine(o_parts, lse_parts):
 # --------------------------------------------------------------------------
 # Whole request from the paged cache (a2 + gather + O7)
 # --------------------------------------------------------------------------
-def decode_request(q_rows, pools, block_table_row, L, softmax_scale, **kw):
-    """q-quant (a2), gather (a4), O7 (a5-a9) for one request.
-    q_rows [H,576] BF16 values.  Returns (o, lse)."""
+def decode_request(q_rows, pools, block_table_row, L, softmax_scale, mx=False, **kw):
+    """q-quant (a2), gather (a4), O7 (a5-a9) for one request; ``mx=True``: the NEXT-4(b)
+    MX variant (decode_mx) instead.  q_rows [H,576] BF16 values.  Returns (o, lse)."""
     qc, sq, qr = q_quant(q_rows)
     kc, sk, kr = gather_request(pools, block_table_row, L)
+    if mx:
+        return decode_mx(qc, sq, qr, kc, sk, kr, softmax_scale, **kw)
     return decode_o7(qc, sq, qr, kc, sk, kr, softmax_scale, **kw)
 
 

@@ -42,11 +42,10 @@
 #include <atomic>
 #include <mutex>
 
-#include "snapmla_internal.h"
+#include "decode_common.cuh"
 
 namespace snapmla {
 
-constexpr int kThreads = 512;     // 16 warps
 constexpr int kWarpAcc = 0;       // 0-3 accumulators, O cols 0-255; 4-7 cols 256-511
 constexpr int kWarpTma = 8;       // 8     TMA producer
 constexpr int kWarpQk = 9;        // 9     QK issuer, owns TMEM
@@ -57,7 +56,6 @@ constexpr int kWarpSoftmax = 12;  // 12-15 softmax
 constexpr uint32_t kRegsAcc = 176, kRegsIssue = 40, kRegsSoftmax = 120;
 constexpr int kPSlots = 2;        // P' + stats ring depth (blocks)
 constexpr int kSSlots = 2;        // S ring depth (TMEM)
-constexpr uint32_t kBoxBytes = 8192;                        // 64 rows x 128 B
 constexpr uint32_t kKvTx = kBc * (kDc + 2 * kDr + 4);       // 41216 B per block
 constexpr uint32_t kStage = 41984;                          // kKvTx rounded up to 1024 (FP8 KV slot)
 constexpr uint32_t kOffQr = 0;                              // [64 rows x 128 B] SW128 (q_r / sigma_q, BF16)
@@ -73,54 +71,6 @@ constexpr uint32_t kIdescQk16 = make_idesc(1, 1, 0, 0, 64, 64);     // BF16 x BF
 constexpr uint32_t kIdescPv = make_idesc(0, 0, 0, 1, 64, 256);      // P' K-major, V MN-major
 constexpr uint32_t kIdescQkB = make_idesc(1, 1, 0, 0, 64, 64);      // BF16 variant: q content x K content
 constexpr uint32_t kIdescPvB = make_idesc(1, 1, 0, 1, 64, 256);     // BF16 variant: P K-major, V MN-major
-
-struct DecodeParams {
-  const __nv_bfloat16* q;
-  const uint8_t* kv_fp8;         // pools (L2 prefetch addresses; the loads go through the tensor maps)
-  const __nv_bfloat16* kv_rope;
-  const float* kv_scale;
-  const int32_t* block_table;
-  const int32_t* seq_lens;
-  const int32_t* ws_hdr;
-  const int32_t* cum;
-  const int32_t* first_req;
-  float* lse_part;
-  float* o_part;
-  int batch, num_heads, n_ht, max_pages;   // num_heads = rows per request = q_len x heads
-  int q_len, heads;                         // MTP: row = t * heads + h for query token t
-  float scale_log2;   // softmax_scale * log2(e)
-  unsigned long long* trace;   // debug timeline (CTA 0), only in SNAPMLA_TRACE builds
-};
-
-// debug timeline (SNAPMLA_TRACE builds only): trace[ev * kTraceN + n] = clock64() of event ev at block n (CTA 0)
-constexpr int kTraceN = 256;
-enum TraceEv { TR_TMA = 0, TR_QK, TR_PVL, TR_PVR, TR_SM_IN, TR_SM_OUT, TR_C_L, TR_C_R, TR_S1, TR_S2, TR_S3, TR_S4, TR_S5, TR_C0, TR_C1, TR_C2, TR_NEV };
-#ifdef SNAPMLA_TRACE
-#define TRACE(ev, n)                                                                          \
-  do {                                                                                        \
-    if (p.trace != nullptr && blockIdx.x == 0 && (n) < (uint32_t)kTraceN)                     \
-      p.trace[(ev) * kTraceN + (n)] = clock64();                                              \
-  } while (0)
-#else
-#define TRACE(ev, n) \
-  do {               \
-  } while (0)
-#endif
-
-// Warp-level arrive on a barrier that publishes (or releases) this warp's SMEM writes (reads):
-// by default lane 0 arrives after __syncwarp (one arrival per warp); a SNAPMLA_LANE_ARRIVE build
-// (compute-sanitizer racecheck runs, scripts/sanitize_all.sh) makes every lane arrive, which the
-// tool models as synchronisation; counts scale by kArriveMul.
-#ifdef SNAPMLA_LANE_ARRIVE
-constexpr uint32_t kArriveMul = 32;
-__device__ __forceinline__ void warp_arrive(uint32_t bar, int) { mbar_arrive(bar); }
-#else
-constexpr uint32_t kArriveMul = 1;
-__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
-  __syncwarp();
-  if (lane == 0) mbar_arrive(bar);
-}
-#endif
 
 struct Bars {
   uint64_t kv_full[5], kv_empty[5];             // TMA -> QK / PV_L + PV_R -> TMA (max over variants)
@@ -217,54 +167,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
   pdl_wait();
 }
 
-// ------------------------------------------------------------------- units
-struct Unit {
-  int b, k0, k1, slot;
-};
-
-struct UnitIter {
-  const int32_t* cum;
-  int lo, hi, g, b, batch;
-  __device__ bool next(Unit& u) {
-    while (b < batch) {
-      const int c0 = __ldg(cum + b), c1 = __ldg(cum + b + 1);
-      if (c0 >= hi) return false;
-      const int k0 = max(lo, c0) - c0, k1 = min(hi, c1) - c0;
-      const int bb = b++;
-      if (k1 > k0) {
-        u.b = bb;
-        u.k0 = k0;
-        u.k1 = k1;
-        u.slot = bb + g;
-        return true;
-      }
-    }
-    return false;
-  }
-};
-
-
-// The TMA producer's page-id loads are a dependent chain (each TMA needs its block-table entry);
-// at a unit start they would cost one DRAM round trip per block (~2K cycles, CTA-0 timeline),
-// so the unit's block-table segment is requested up front, one L1 prefetch per 128-byte line.
-__device__ __forceinline__ void prefetch_block_table(const int32_t* bt, int k0, int k1) {
-  for (int j = k0 & ~31; j < k1; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(bt + j));
-}
-
 // ------------------------------------------------------------- decode kernel
-// x / s for a row-constant s: rcp + one FMA correction of the quotient
-// (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
-__device__ __forceinline__ float div_by(float x, float s, float rs) {
-  const float q = x * rs;
-  return fmaf(fmaf(-q, s, x), rs, q);
-}
-// the same on a pair, packed f32x2 (bit-identical to two div_by calls: fma(q, -s, x) == fma(-q, s, x))
-__device__ __forceinline__ float2 div_by2(float2 x, float s, float rs) {
-  const float2 rs2 = make_float2(rs, rs), ns2 = make_float2(-s, -s);
-  const float2 q = __fmul2_rn(x, rs2);
-  return __ffma2_rn(__ffma2_rn(q, ns2, x), rs2, q);
-}
-
 // One QK block into S (TMEM): 16 x kind::f8f6f4 (K = 32) over the 512 content dims,
 // then 4 x kind::f16 (K = 16) over the 64 RoPE dims, accumulating into the same S;
 // commit to `bar`.  One elect for the whole block.  Descriptor start addresses
@@ -1611,7 +1514,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 // ---- process-wide host state (thread-safe): the debug switches below, a per-device
 // record of one-time launch attributes, and a small cache of encoded tensor maps keyed by
 // (device, pool base, rows, kind).  Nothing else is global.
-static std::atomic<unsigned long long*> g_trace{nullptr};
+std::atomic<unsigned long long*> g_trace{nullptr};
 static std::atomic<int> g_kernel{-1};   // 64 < rows <= 128: -1 auto, 0 single-CTA, 1 block-pair (debug override)
 
 struct DeviceInfo {
@@ -1634,7 +1537,7 @@ constexpr int kTmapCache = 32;
 static TmapEntry g_tmap[kTmapCache];
 static int g_tmap_n = 0, g_tmap_next = 0;
 
-static int current_device() {
+int current_device() {
   int dev = 0;
   return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kMaxDevices ? dev : -1;
 }
@@ -1652,7 +1555,7 @@ int device_num_sms() {
 }
 
 // the encoded map for (current device, base, rows, kind), encoding it on first use
-static bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap* out) {
+bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap* out) {
   std::lock_guard<std::mutex> lk(g_host_mu);
   for (int i = 0; i < g_tmap_n; ++i) {
     const TmapEntry& e = g_tmap[i];
@@ -1672,6 +1575,23 @@ static bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUte
   if (g_tmap_n < kTmapCache) ++g_tmap_n;
   *out = m;
   return true;
+}
+
+mla_status launch_plan(const int32_t* seq_lens, int batch, int num_heads, int groups, int32_t* hdr, int32_t* cum,
+                       int32_t* first_req, int num_sms, cudaStream_t st) {
+  cudaLaunchAttribute pdl_attr[1];
+  pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t pc = {};
+  pc.gridDim = dim3(1);
+  pc.blockDim = dim3(1024);
+  pc.stream = st;
+  pc.attrs = pdl_attr;
+  pc.numAttrs = 1;
+  return cudaLaunchKernelEx(&pc, plan_kernel, seq_lens, batch, num_heads, groups, hdr, cum, first_req, num_sms) ==
+                 cudaSuccess
+             ? MLA_OK
+             : MLA_ERR_CUDA;
 }
 
 // one-time per device: dynamic SMEM attribute of a kernel (and the block-pair cluster occupancy)
@@ -1761,19 +1681,7 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   int32_t* cum = reinterpret_cast<int32_t*>(ws + wl.cum);
   int32_t* first = reinterpret_cast<int32_t*>(ws + wl.first);
   cudaStream_t st = (cudaStream_t)stream;
-  cudaLaunchAttribute pdl_attr[1];
-  pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
-  {
-    cudaLaunchConfig_t pc = {};
-    pc.gridDim = dim3(1);
-    pc.blockDim = dim3(1024);
-    pc.stream = st;
-    pc.attrs = pdl_attr;
-    pc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&pc, plan_kernel, seq_lens, batch, num_heads, groups, hdr, cum, first, sms) != cudaSuccess)
-      return MLA_ERR_CUDA;
-  }
+  if (launch_plan(seq_lens, batch, num_heads, groups, hdr, cum, first, sms, st) != MLA_OK) return MLA_ERR_CUDA;
 
   const uint32_t smem = bp ? kBpSmem : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
   DecodeParams prm;

@@ -87,7 +87,10 @@ DEVI void mbar_wait(uint32_t a, uint32_t parity, int tag = -1, int idx = -1) {
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
     if (clock64() - t0 > (1ll << 31)) {
-      printf("HANG block %d thread %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x, tag, idx, parity);
+      unsigned long long raw;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(a));
+      printf("HANG block %d thread %d tag %d idx %d parity %u bar 0x%x raw 0x%016llx\n", blockIdx.x, threadIdx.x, tag,
+             idx, parity, a, raw);
       __trap();
     }
   }

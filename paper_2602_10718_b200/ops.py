@@ -47,6 +47,8 @@ def lib():
     L.mla_decode_fp8.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
     L.mla_decode_fp8_ex.restype = _I
     L.mla_decode_fp8_ex.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
+    L.mla_decode_fp8_mx.restype = _I
+    L.mla_decode_fp8_mx.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I64, _F, _P, _SZ, _P]
     L.mla_kv_fetch_dequant.restype = _I
     L.mla_kv_fetch_dequant.argtypes = [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I64, _I64, _P, _P, _P]
     L.mla_combine.restype = _I
@@ -65,7 +67,7 @@ def lib():
 
 def exported_symbols():
     return ["mla_status_str", "mla_abi_version", "mla_kv_append_quant", "mla_decode_workspace_bytes",
-            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant",
+            "mla_decode_fp8", "mla_decode_fp8_ex", "mla_decode_fp8_mx", "mla_combine", "mla_combine_f32", "mla_kv_fetch_dequant",
             "mla_kv_append_bf16", "mla_decode_bf16", "mla_combine_gather"]
 
 
@@ -127,6 +129,21 @@ def mla_decode_fp8_ex(q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, softm
         batch, num_heads, q_len, D_C, D_R, kv_fp8.shape[1], block_table.shape[1], kv_fp8.shape[0],
         float(softmax_scale), _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
         _stream(stream)), "mla_decode_fp8_ex")
+
+
+def mla_decode_fp8_mx(q, kv_fp8, kv_rope, kv_scale, block_table, seq_lens, softmax_scale, workspace,
+                      stream=None):
+    """NEXT-4(b) MX-scaled P variant (not the paper's method): q bf16 [batch, num_heads, 576] or
+    [batch, q_len, num_heads, 576], q_len x num_heads <= 128; partials in `workspace` as mla_decode_fp8_ex."""
+    batch = q.shape[0]
+    q_len, num_heads = (q.shape[1], q.shape[2]) if q.dim() == 4 else (1, q.shape[1])
+    _check(lib().mla_decode_fp8_mx(
+        _dev(q, torch.bfloat16, "q"), _dev(kv_fp8, torch.uint8, "kv_fp8"),
+        _dev(kv_rope, torch.bfloat16, "kv_rope"), _dev(kv_scale, torch.float32, "kv_scale"),
+        _dev(block_table, torch.int32, "block_table"), _dev(seq_lens, torch.int32, "seq_lens"),
+        batch, num_heads, q_len, D_C, D_R, kv_fp8.shape[1], block_table.shape[1], kv_fp8.shape[0],
+        float(softmax_scale), _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream)), "mla_decode_fp8_mx")
 
 
 def mla_combine(workspace, batch, num_heads, out, lse=None, stream=None):
@@ -229,9 +246,10 @@ class PagedMLACache:
 
 
 def decode_step(q, cache, block_table, seq_lens, softmax_scale, workspace=None, out=None, lse=None,
-                stream=None, f32_out=False):
+                stream=None, f32_out=False, mx=False):
     """mla_decode_fp8 (q [B, H, 576]) or mla_decode_fp8_ex (q [B, q_len, H, 576], MTP) + mla_combine;
-    mla_decode_bf16 when `cache` is a PagedMLACacheBF16 (NEXT-2 baseline).
+    mla_decode_bf16 when `cache` is a PagedMLACacheBF16 (NEXT-2 baseline); mla_decode_fp8_mx with
+    mx=True (NEXT-4(b) variant).
     Returns (out, lse) shaped like q's leading dims."""
     lead = tuple(q.shape[:-1])
     batch, rows = q.shape[0], 1
@@ -243,7 +261,10 @@ def decode_step(q, cache, block_table, seq_lens, softmax_scale, workspace=None, 
         out = torch.empty(lead + (D_C,), dtype=torch.float32 if f32_out else torch.bfloat16, device=q.device)
     if lse is None:
         lse = torch.empty(lead, dtype=torch.float32, device=q.device)
-    if isinstance(cache, PagedMLACacheBF16):
+    if mx:
+        mla_decode_fp8_mx(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,
+                          workspace, stream)
+    elif isinstance(cache, PagedMLACacheBF16):
         mla_decode_bf16(q, cache.kv_c, cache.kv_rope, block_table, seq_lens, softmax_scale, workspace, stream)
     elif q.dim() == 4:
         mla_decode_fp8_ex(q, cache.kv_fp8, cache.kv_rope, cache.kv_scale, block_table, seq_lens, softmax_scale,

@@ -76,7 +76,7 @@ class Case:
         """O7 per query token over its causally visible keys (reading R25)."""
         return O.decode_request_mtp(self.q[b].float().numpy(), pools, self.bt[b], int(self.lens[b]), self.scale)
 
-    def oracle_request(self, pools, b, heads=None, which="o7"):
+    def oracle_request(self, pools, b, heads=None, which="o7", mx=False):
         L = int(self.lens[b])
         q = self.q[b].float().numpy()
         if heads is not None:
@@ -88,6 +88,8 @@ class Case:
         kc, sk, kr = O.gather_request(pools, self.bt[b], L)
         if which == "o6":
             return O.attn_o6(qc, sq, qr, kc, sk, kr, self.scale)
+        if mx:   # NEXT-4(b) variant (test_gpu_mx.py)
+            return O.decode_mx(qc, sq, qr, kc, sk, kr, self.scale)
         return O.decode_o7(qc, sq, qr, kc, sk, kr, self.scale)
 
 
