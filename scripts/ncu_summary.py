@@ -77,8 +77,24 @@ def launch_shares(path):
     return {k: (v, v / tot) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])}, tot
 
 
+def commit_hash():
+    try:
+        return subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
+                              cwd=ROOT).stdout.strip() or None
+    except OSError:
+        return None
+
+
+def kernel_name(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, vals = rows[0], rows[2]
+    return vals[hdr.index("Kernel Name")].split("(")[0] if "Kernel Name" in hdr else None
+
+
 def main():
     tag, works = sys.argv[1], sys.argv[2:]
+    commit = os.environ.get("NCU_COMMIT") or commit_hash()
     os.makedirs(PROF, exist_ok=True)
     sp = os.path.join(PROF, "ncu_decode_summary.json")
     summary = json.load(open(sp)) if os.path.exists(sp) else {}
@@ -90,6 +106,8 @@ def main():
         dur = to_si(*m["gpu__time_duration.sum"])
         entry = {
             "round": tag,
+            "commit": commit,
+            "kernel": kernel_name(rep),
             "dram_bytes_per_launch": rd + wr,
             "dram_read_bytes": rd,
             "dram_write_bytes": wr,
@@ -113,7 +131,8 @@ def main():
             for k, (v, f) in shares.items():
                 lines.append(f"{k[:80]:80s} {v:.6e} {100 * f:5.1f}%")
             entry["decode_share_of_step_ncu"] = next((f for k, (v, f) in shares.items() if "mla_decode_" in k), None)
-        summary[w + ("_bf16" if "bf16" in tag else "")] = entry   # the BF16 baseline keeps its own key
+        key = w + ("_bf16" if "bf16" in tag else "") + ("_mx" if "mx" in tag else "")   # variants keep their own key
+        summary[key] = entry
         open(os.path.join(PROF, f"{tag}_ncu_{w}.txt"), "w").write("\n".join(lines) + "\n")
         print(w, json.dumps(entry))
     json.dump(summary, open(sp, "w"), indent=1)
