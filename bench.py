@@ -118,6 +118,9 @@ def init_dist(world, local_rank):
         if oversub:
             dist.init_process_group("gloo")
         else:
+            # communicator log on stderr (comm nRanks, NVLS / P2P transport) for the driver to check
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
     return dev_idx, oversub
 
@@ -413,6 +416,16 @@ def run_ours(args, rank, world, local_rank):
         sl_v = (pos % 64 + 1).to(torch.int32)
         c, r = synth.torch_latent(idx.numel(), gen, dev)
         cache.append(c, r, bt_v, sl_v)
+    if tp_world > 1:   # the ranks of a TP group must hold byte-identical caches (same seed, same appends)
+        planes = [cache.kv_c] if args.bf16 else [cache.kv_fp8, cache.kv_scale]
+        planes += [cache.kv_rope, block_table]
+        ck = torch.stack([x.contiguous().view(torch.int32).sum(dtype=torch.int64) for x in planes])
+        ck = ck.to("cpu" if oversub else dev)
+        lo_ck, hi_ck = ck.clone(), ck.clone()
+        dist.all_reduce(lo_ck, op=dist.ReduceOp.MIN, group=tp_group)
+        dist.all_reduce(hi_ck, op=dist.ReduceOp.MAX, group=tp_group)
+        if not torch.equal(lo_ck, hi_ck):
+            raise SystemExit(f"rank {rank}: TP replicas hold different KV caches")
     if T == 1:
         q_all = synth.torch_queries(B * H, gen, dev).view(B, H, 576)
         q = q_all[:, head0:head1].contiguous()
