@@ -922,6 +922,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
+#ifdef SNAPMLA_TRACE
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x] = gt;
+  }
+#endif
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kBpSlots; ++i) {
@@ -1478,6 +1485,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     tc_fence_after();
     tmem_dealloc_pair(tmem, 512);
   }
+#ifdef SNAPMLA_TRACE
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    p.trace[TR_NEV * kTraceN + 2 * blockIdx.x + 1] = gt;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ host side

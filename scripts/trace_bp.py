@@ -47,8 +47,28 @@ ct = tr.cpu().numpy()[16 * 256:].reshape(-1, 2).astype(np.int64)
 ok = ct[:, 0] > 0
 if ok.any():
     d = (ct[ok, 1] - ct[ok, 0]) / 1e3
-    print("CTA durations us: min/median/max", d.min(), np.median(d), d.max(), "span", (ct[ok, 1].max() - ct[ok, 0].min()) / 1e3)
+    t0 = ct[ok, 0].min()
+    print("CTA durations us: min/median/max", d.min(), np.median(d), d.max(), "span", (ct[ok, 1].max() - t0) / 1e3)
+    print("CTA start offsets us: median/max", np.median((ct[ok, 0] - t0) / 1e3), ((ct[ok, 0] - t0) / 1e3).max())
+    ends = np.sort((ct[ok, 1] - t0) / 1e3)
+    print("CTA end times us (sorted, every 16th):", [round(x, 1) for x in ends[::16]], "last", round(ends[-1], 1))
+    ws = torch.zeros(8, dtype=torch.int32)
+    hdr = None
+    try:
+        nsm = torch.cuda.get_device_properties(0).multi_processor_count
+        print("SMs", nsm, "CTAs traced", int(ok.sum()))
+    except Exception as e:
+        print(e)
 rel = t - t[N["TMA"]][0]
 print("first pairs (TMA, QK, SM_in, SM_out, PVL, C_L):")
 for n in range(min(nv, 6)):
     print(n, [int(rel[N[e]][n]) for e in ("TMA", "QK", "SM_in", "SM_out", "PVL", "C_L")])
+# untraced decode time of the same call (trace buffer off)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for i in range(3):
+    ops.decode_step(q, cache, bt, sl, synth.DEFAULT_SOFTMAX_SCALE)
+e0.record()
+for i in range(20):
+    ops.decode_step(q, cache, bt, sl, synth.DEFAULT_SOFTMAX_SCALE)
+e1.record(); torch.cuda.synchronize()
+print("untraced decode_step ms (mean of 20):", round(e0.elapsed_time(e1) / 20, 4))
