@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsnapmla.so")
-SOURCES = ["append.cu", "decode.cu", "decode_mx.cu", "combine.cu", "fetch.cu", "measure.cu"]
+SOURCES = ["append.cu", "decode.cu", "decode_sw.cu", "decode_mx.cu", "combine.cu", "fetch.cu", "measure.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

@@ -1530,6 +1530,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 // (device, pool base, rows, kind).  Nothing else is global.
 std::atomic<unsigned long long*> g_trace{nullptr};
 static std::atomic<int> g_kernel{-1};   // 64 < rows <= 128: -1 auto, 0 single-CTA, 1 block-pair (debug override)
+static std::atomic<int> g_small{-1};    // rows <= 32: -1 auto (swapped-operand kernel), 0 single-CTA (debug override)
 
 struct DeviceInfo {
   int sms = 0;
@@ -1626,6 +1627,8 @@ using namespace snapmla;
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace.store(dev_buf); }
 // Debug / test only: force the kernel for 64 < rows <= 128 (-1 = automatic, the default).
 extern "C" void mla_debug_set_pair(int v) { g_kernel.store(v); }
+// Debug / test only: rows <= 32 run the swapped-operand kernel (-1, the default) or the single-CTA one (0).
+extern "C" void mla_debug_set_small(int v) { g_small.store(v); }
 extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms) {
   if (batch < 0 || num_heads <= 0) return 0;
   if (num_sms <= 0) num_sms = device_num_sms();
@@ -1666,6 +1669,7 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   const int force = g_kernel.load();
   const bool bp = !bf16 && n_ht == 2 &&
                   (force == 1 || (force < 0 && (int64_t)batch * max_pages_per_seq >= kBpMinBlocks));
+  const bool sw = !bf16 && num_heads <= 32 && g_small.load() != 0;
   int groups = sms / n_ht;
   if (bp) {
     if (!ensure_attr(dev, 2, mla_decode_bp_kernel, kBpSmem)) return MLA_ERR_CUDA;
@@ -1681,7 +1685,7 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
     }
     const int nc = g_dev[dev].bp_max_clusters;
     if (nc > 0 && nc < groups) groups = nc;
-  } else if (!(bf16 ? ensure_attr(dev, 1, mla_decode_kernel<true>, Variant<true>::kSmem)
+  } else if (!sw && !(bf16 ? ensure_attr(dev, 1, mla_decode_kernel<true>, Variant<true>::kSmem)
                     : ensure_attr(dev, 0, mla_decode_kernel<false>, Variant<false>::kSmem))) {
     return MLA_ERR_CUDA;
   }
@@ -1718,6 +1722,9 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   prm.max_pages = max_pages_per_seq;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
   prm.trace = g_trace.load();
+  if (sw) return launch_decode_sw(tm_kv, tm_rope, prm, dev, sms, st) == MLA_OK && cudaGetLastError() == cudaSuccess
+                     ? MLA_OK
+                     : MLA_ERR_CUDA;
   // programmatic dependent launch: the decode CTAs start (barrier init, TMEM
   // alloc, descriptor prefetch) while the plan kernel runs; griddepcontrol.wait
   // in the kernel orders every read of the plan / cache after it.

@@ -111,6 +111,9 @@ mla_status launch_plan(const int32_t* seq_lens, int batch, int num_heads, int gr
 // the encoded TMA map of a pool (cached per device; kind 0 FP8 content, 1 BF16 content, 2 RoPE)
 bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap* out);
 int current_device();
+// the swapped-operand kernel for rows <= 32 (decode_sw.cu); the plan has been launched
+mla_status launch_decode_sw(const CUtensorMap& tm_kv, const CUtensorMap& tm_rope, const DecodeParams& prm, int dev,
+                            int sms, cudaStream_t st);
 extern std::atomic<unsigned long long*> g_trace;
 
 }  // namespace snapmla
