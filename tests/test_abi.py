@@ -47,7 +47,8 @@ def test_debug_header_symbols_exported(L):
     from paper_2602_10718_b200 import ops
     src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "snapmla_debug.h")).read(), flags=re.S)
     names = sorted(set(re.findall(r"\b(mla_[a-z0-9_]+)\s*\(", src)))
-    assert names == ["mla_debug_cvt_e4m3", "mla_debug_set_pair", "mla_debug_set_trace", "mla_measure_read_stream"]
+    assert names == ["mla_debug_cvt_e4m3", "mla_debug_set_pair", "mla_debug_set_small", "mla_debug_set_trace",
+                     "mla_measure_read_stream"]
     out = subprocess.run(["nm", "-D", "--defined-only", ops.LIB_PATH], capture_output=True, text=True).stdout
     for name in names:
         assert re.search(r"\bT " + name + r"\b", out), name
