@@ -71,6 +71,8 @@ def parse():
                     help="tp / dptp: all-gather fused into the combine epilogue (mla_combine_gather, symmetric memory)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every step's kernels from the host instead of replaying a CUDA graph of one step")
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs: no clock-settle loop, no e2e leg, no cpu baseline")
     ap.add_argument("--mtp", type=int, default=1, help="query tokens per request per step (MTP, NEXT-1)")
@@ -507,10 +509,21 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # One step (append x T -> plan -> decode -> combine, PDL-chained) captured once into a CUDA graph and
+    # replayed: the host launches one graph per step instead of T + 3 kernels, so small shapes are no
+    # longer launch-bound.  Not with TP collectives in the step (NCCL / peer barriers stay eager).
+    graph = None
+    if not args.no_graph and tp_world == 1:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+    run_step = graph.replay if graph is not None else step
     t_settle = time.time()
     while not args.quick and time.time() - t_settle < 1.0:        # keep the GPU loaded so clocks are sampled under load
         for _ in range(10):
-            step()
+            run_step()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -519,7 +532,7 @@ def run_ours(args, rank, world, local_rank):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(args.steps):
-        step()          # no events between the kernels of the timed steps (an event record breaks the PDL overlap)
+        run_step()      # no events between the kernels of the timed steps (an event record breaks the PDL overlap)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -552,7 +565,8 @@ def run_ours(args, rank, world, local_rank):
         return {"metric": METRIC, "value": round(tokens_per_step / (ms_step / 1e3), 1),
                 "unit": "tokens/s", "ms_per_step": ms_step, "decode_ms": dec_ms, "quick": True,
                 "batch": B, "global_batch": B_global, "heads": H, "context": L, "mtp": T, "n_gpus": world,
-                "roofline_frac": round(achieved / peak, 4), "achieved_gbs": round(achieved, 1), "clocks": clk}
+                "roofline_frac": round(achieved / peak, 4), "achieved_gbs": round(achieved, 1), "clocks": clk,
+                "launch": "cuda_graph" if graph is not None else "eager"}
 
     # ---------------- e2e: host buffers through the public API
     q_h = q.cpu().pin_memory()
@@ -700,6 +714,8 @@ def run_ours(args, rank, world, local_rank):
                         "(read-back stream) overlap the compute of step i; double-buffered",
                 "serial_value": round(tokens_per_step / (e_ms / args.steps / 1e3), 1)},
         "gpu_launches": launches_per_step * args.steps,
+        "launch": ("CUDA graph of one step (T + 3 kernels, PDL edges), replayed per timed step" if graph is not None
+                   else "eager (host launches every kernel)"),
         "clocks": clk,
         "clocks_e2e": clk_e2e,
         "peaks_measured": peaks,

@@ -1,6 +1,7 @@
 // a10: split-KV combine (Algorithm 1 returns o and the logsumexp L).
 //   L = log sum_s e^{L_s};   o = sum_s e^{L_s - L} o_s
-// One warp per (request, head); lane l owns output columns [16l, 16l+16).
+// One warp per (request, head, quarter of the 512 columns); lane l owns 4 columns; the split LSEs and
+// weights are handled lane-parallel, eight splits' partial rows are in flight at a time.
 // The split list of request b is the contiguous slot range b + g for the
 // groups g that the decode plan assigned to b's key blocks.
 #include "snapmla_internal.h"
@@ -17,14 +18,17 @@ struct Peers {
   int world, rank;
 };
 
-template <bool kF32Out, bool kGather = false>
+// kQ warps per (request, head) row, each owning 512 / kQ columns (kQ = 4 when requests have many
+// splits -- small batches -- so more partial loads are in flight; kQ = 1 otherwise).
+template <bool kF32Out, bool kGather = false, int kQ = 1>
 __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ ws, size_t off_cum, size_t off_lse,
                                                       size_t off_o, int batch, int num_heads, int num_sms,
                                                       void* __restrict__ out, float* __restrict__ lse_out,
                                                       const Peers peers = Peers{}) {
   pdl_wait();   // launched as a programmatic dependent of the decode: its partials are complete here
   const int lane = threadIdx.x & 31;
-  const int idx = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int widx = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int idx = widx / kQ, qc = widx % kQ;   // row (request, head) and its share of the 512 columns
   if (idx >= batch * num_heads) return;
   const int b = idx / num_heads, h = idx % num_heads;
   const int32_t* hdr = reinterpret_cast<const int32_t*>(ws);
@@ -39,65 +43,91 @@ __global__ void __launch_bounds__(128) combine_kernel(const char* __restrict__ w
   const int per = hdr[H_PER], n_ht = hdr[H_NHT];
   const int c0 = cum[b], c1 = cum[b + 1];
   const int ht = h / kHeadTile, row = h % kHeadTile;
+  constexpr int kV = 4 / kQ;              // float4 per lane per split
+  constexpr int kIn = 8 / kV;              // splits' partial rows in flight
+  const int col = (512 / kQ) * qc + 4 * kV * lane;   // this lane's 4 kV output columns
 
-  float acc[16];
+  float4 acc[kV];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  for (int e = 0; e < kV; ++e) acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   float lse = -INFINITY;
   if (c1 > c0) {
-    int g0 = c0 / per, g1 = (c1 - 1) / per;
+    const int g0 = c0 / per, g1 = (c1 - 1) / per;
+    int ns = g1 - g0 + 1;   // splits of request b
+    const int64_t sstride = (int64_t)n_ht * kHeadTile;   // rows between consecutive splits' partials
+    const float* lse_row = lse_p + ((int64_t)(b + g0) * n_ht + ht) * kHeadTile + row;
+    // the split LSEs are read lane-parallel (a serial loop over many splits -- small batches split
+    // over all CTA groups -- is a chain of dependent memory latencies)
     float mx = -INFINITY;
-    for (int g = g0; g <= g1; ++g) mx = fmaxf(mx, lse_p[((int64_t)(b + g) * n_ht + ht) * kHeadTile + row]);
-    if (mx == -INFINITY) g1 = g0 - 1;   // the row saw no key at all (MTP token beyond a short cache)
-    float wsum = 0.f;
-    for (int g = g0; g <= g1; ++g) {
-      const int64_t pr = ((int64_t)(b + g) * n_ht + ht) * kHeadTile + row;
-      const float w = expf(lse_p[pr] - mx);
-      wsum += w;
-      const float4* src = reinterpret_cast<const float4*>(o_p + pr * kDc + lane * 16);
+    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, lse_row[s * sstride]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 v = src[i];
-        acc[4 * i + 0] = fmaf(w, v.x, acc[4 * i + 0]);
-        acc[4 * i + 1] = fmaf(w, v.y, acc[4 * i + 1]);
-        acc[4 * i + 2] = fmaf(w, v.z, acc[4 * i + 2]);
-        acc[4 * i + 3] = fmaf(w, v.w, acc[4 * i + 3]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (mx == -INFINITY) ns = 0;   // the row saw no key at all (MTP token beyond a short cache)
+    float wsum = 0.f;
+    const float* src0 = o_p + (((int64_t)(b + g0) * n_ht + ht) * kHeadTile + row) * kDc + col;
+    for (int s0 = 0; s0 < ns; s0 += 32) {
+      const float wl = s0 + lane < ns ? expf(lse_row[(s0 + lane) * sstride] - mx) : 0.f;
+      wsum += wl;
+      const int cnt = min(32, ns - s0);
+      const float* src = src0 + (int64_t)s0 * sstride * kDc;
+      int i = 0;
+      for (; i + kIn <= cnt; i += kIn) {   // kIn splits' partial rows in flight, accumulated in split order
+        float4 v[kIn][kV];
+#pragma unroll
+        for (int k = 0; k < kIn; ++k)
+#pragma unroll
+          for (int e = 0; e < kV; ++e)
+            v[k][e] = reinterpret_cast<const float4*>(src + (int64_t)(i + k) * sstride * kDc)[e];
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+          const float w = __shfl_sync(0xffffffffu, wl, i + k);
+#pragma unroll
+          for (int e = 0; e < kV; ++e)
+            acc[e] = make_float4(fmaf(w, v[k][e].x, acc[e].x), fmaf(w, v[k][e].y, acc[e].y), fmaf(w, v[k][e].z, acc[e].z),
+                                 fmaf(w, v[k][e].w, acc[e].w));
+        }
+      }
+      for (; i < cnt; ++i) {
+        const float w = __shfl_sync(0xffffffffu, wl, i);
+#pragma unroll
+        for (int e = 0; e < kV; ++e) {
+          const float4 v = reinterpret_cast<const float4*>(src + (int64_t)i * sstride * kDc)[e];
+          acc[e] = make_float4(fmaf(w, v.x, acc[e].x), fmaf(w, v.y, acc[e].y), fmaf(w, v.z, acc[e].z), fmaf(w, v.w, acc[e].w));
+        }
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
     if (wsum > 0.f) {
       const float inv = 1.0f / wsum;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] *= inv;
+      for (int e = 0; e < kV; ++e) acc[e] = make_float4(acc[e].x * inv, acc[e].y * inv, acc[e].z * inv, acc[e].w * inv);
       lse = mx + logf(wsum);
     }
   }
-  const int64_t orow = (int64_t)idx * kDc + lane * 16;
+  const int64_t orow = (int64_t)idx * kDc + col;
   if constexpr (kF32Out) {
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + orow);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+    for (int e = 0; e < kV; ++e) reinterpret_cast<float4*>(static_cast<float*>(out) + orow)[e] = acc[e];
   } else {
-    uint32_t wv[8];
+    uint2 wv[kV];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      __nv_bfloat162 v = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
-      wv[i] = *reinterpret_cast<uint32_t*>(&v);
+    for (int e = 0; e < kV; ++e) {
+      __nv_bfloat162 v0 = __floats2bfloat162_rn(acc[e].x, acc[e].y), v1 = __floats2bfloat162_rn(acc[e].z, acc[e].w);
+      wv[e] = make_uint2(*reinterpret_cast<uint32_t*>(&v0), *reinterpret_cast<uint32_t*>(&v1));
     }
     if constexpr (kGather) {
       // row (b, rank * num_heads + h) of the [batch, world * num_heads, 512] output of every rank
-      const int64_t grow = ((int64_t)b * peers.world * num_heads + (int64_t)peers.rank * num_heads + h) * kDc + lane * 16;
-      for (int r = 0; r < peers.world; ++r) {
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(peers.out[r]) + grow);
-        dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-      }
+      const int64_t grow = ((int64_t)b * peers.world * num_heads + (int64_t)peers.rank * num_heads + h) * kDc + col;
+      for (int r = 0; r < peers.world; ++r)
+#pragma unroll
+        for (int e = 0; e < kV; ++e) reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(peers.out[r]) + grow)[e] = wv[e];
     } else {
-      uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + orow);
-      dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+#pragma unroll
+      for (int e = 0; e < kV; ++e) reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + orow)[e] = wv[e];
     }
   }
-  if (lse_out && lane == 0) lse_out[idx] = lse;
+  if (lse_out && lane == 0 && qc == 0) lse_out[idx] = lse;
 }
 
 // programmatic dependent launch (the kernel's griddepcontrol.wait orders it after the decode)
@@ -128,9 +158,13 @@ static mla_status launch_combine(const void* workspace, int batch, int num_heads
   const int sms = device_num_sms();
   if (sms <= 0) return MLA_ERR_CUDA;
   const WsLayout wl = ws_layout(batch, num_heads, sms);
-  const int n = batch * num_heads;
-  return launch_pdl(combine_kernel<kF32>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum, wl.lse,
-                    wl.o, batch, num_heads, sms, out, lse, Peers{});
+  const int n = batch * num_heads;   // rows
+  const int groups = sms / ((num_heads + kHeadTile - 1) / kHeadTile);
+  if (2 * batch < groups)   // several splits per request: 4 warps per row (4 warps per CTA)
+    return launch_pdl(combine_kernel<kF32, false, 4>, n, stream, static_cast<const char*>(workspace), wl.cum, wl.lse,
+                      wl.o, batch, num_heads, sms, out, lse, Peers{});
+  return launch_pdl(combine_kernel<kF32, false, 1>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum,
+                    wl.lse, wl.o, batch, num_heads, sms, out, lse, Peers{});
 }
 
 }  // namespace snapmla
@@ -160,7 +194,7 @@ extern "C" mla_status mla_combine_gather(const void* workspace, int batch, int n
   if (sms <= 0) return MLA_ERR_CUDA;
   const WsLayout wl = ws_layout(batch, num_heads, sms);
   const int n = batch * num_heads;
-  return launch_pdl(combine_kernel<false, true>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum,
+  return launch_pdl(combine_kernel<false, true, 1>, (n + 3) / 4, stream, static_cast<const char*>(workspace), wl.cum,
                     wl.lse, wl.o, batch, num_heads, sms, static_cast<void*>(nullptr), lse, peers);
 }
 

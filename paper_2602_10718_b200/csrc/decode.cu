@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
   if (tid == 1023) {
     const int total = warp_sums[31];
     cum[batch] = total;
-    const int per = total > 0 ? (total + groups - 1) / groups : 1;
+    // at least kMinPer blocks per CTA group: a small problem spread one block per group writes (and
+    // the combine reads) a 64-row fp32 partial per block -- more bytes than the block's KV itself
+    constexpr int kMinPer = 4;
+    const int per = total > 0 ? max((total + groups - 1) / groups, kMinPer) : 1;
     s_per = per;
     hdr[H_TOTAL] = total;
     hdr[H_PER] = per;
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t bar0 = sbase + V::kOffBar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(TR_C2, 250u);   // prologue stamps (trace builds): kernel entry
 
   // ---- setup overlaps the plan kernel (programmatic dependent launch)
   if (threadIdx.x == 0) {
@@ -336,8 +340,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = lds_u32(BAR(tmem_base));
   const uint32_t tmem_S = tmem;                       // lanes 0-15 (+32k): S slot s at cols 64 s
 
+  if (threadIdx.x == 0) TRACE(TR_C2, 251u);   // setup done
   pdl_wait();   // plan (and the appends before it) visible from here on
   pdl_launch_dependents();   // the combine may be scheduled as CTAs retire (it waits for completion)
+  if (threadIdx.x == 0) TRACE(TR_C2, 252u);   // plan visible
   const int ht = blockIdx.x % p.n_ht;
   const int g = blockIdx.x / p.n_ht;
   const int per = p.ws_hdr[H_PER], total = p.ws_hdr[H_TOTAL], groups = p.ws_hdr[H_GROUPS];
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
         mbar_wait(BAR(q_full), unit & 1, 2, unit);
+        if (lane == 0 && unit == 0) TRACE(TR_C2, 254u);   // QK warp: q_full seen
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % V::kSlots, ss = n % kSSlots;
           mbar_wait(BAR(kv_full) + 8 * st, (n / V::kSlots) & 1, 3, n);
@@ -446,6 +453,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n = 0, unit = 0;
     while (it.next(u)) {
       // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh
+      if (row_ok) {   // this thread's q lines to L2 up front: the register-limited load rounds below then hit L2
+        const char* qb = reinterpret_cast<const char*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + 512 * hh + 128 * l));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + 1024 + 64 * hh));
+      }
       if (unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // QK of the previous unit done
       float c_row;
       if constexpr (kBf) {
@@ -540,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(q_full));
+        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 253u);   // Q-quant done (warp 12)
       }
 
       // visible keys of this row: query token t = head / heads of q_len sees the cache

@@ -64,3 +64,9 @@ def med(a, b):
     return np.median((t[b] - t[a])[20:nv])
 print("softmax: S1-SM_in", med(4, 8), "S2-S1", med(8, 9), "S3-S2", med(9, 10), "S4-S3", med(10, 11), "S5-S4", med(11, 12), "SM_out-S5", med(12, 5))
 print("corr: C0-prevC_R", np.median((t[13][21:nv] - t[7][20:nv-1])), "C1-C0", med(13, 14), "C_L-C1", med(14, 6), "C2-C_L", med(6, 15), "C_R-C2", med(15, 7))
+
+pro = tr.cpu().numpy()[15 * 256 + 250: 15 * 256 + 255].astype(np.int64)
+if pro[0] > 0:
+    print("prologue (cycles from kernel entry): setup done", pro[1] - pro[0], "plan visible", pro[2] - pro[0],
+          "Q-quant done", pro[3] - pro[0], "QK sees q_full", pro[4] - pro[0],
+          "first TMA", int(t[0][0] - pro[0]), "first QK", int(t[1][0] - pro[0]), "first SM_in", int(t[4][0] - pro[0]))
