@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_S = tmem;                       // lanes 0-15 (+32k): S slot s at cols 64 s
 
   if (threadIdx.x == 0) TRACE(TR_C2, 251u);   // setup done
+  prefetch_q_slice(p);
   pdl_wait();   // plan (and the appends before it) visible from here on
   pdl_launch_dependents();   // the combine may be scheduled as CTAs retire (it waits for completion)
   if (threadIdx.x == 0) TRACE(TR_C2, 252u);   // plan visible
@@ -491,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(q_full));
       } else {
+        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 245u);   // Q-quant start
         const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
         float amax = 0.f;
 #pragma unroll
@@ -509,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
+        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 246u);   // amax done
         const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
         const float rsq = __frcp_rn(sq);
         c_row = sq * p.scale_log2;
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
         }
         tmem_wait_st();
+        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 247u);   // codes in TMEM
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
           const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
@@ -981,6 +985,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = lds_u32(BP(tmem_base));
 
+  prefetch_q_slice(p);
   pdl_wait();
   pdl_launch_dependents();
   const int ht = (int)cta;

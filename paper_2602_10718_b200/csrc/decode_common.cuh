@@ -91,6 +91,22 @@ __device__ __forceinline__ void prefetch_block_table(const int32_t* bt, int k0, 
   for (int j = k0 & ~31; j < k1; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(bt + j));
 }
 
+// Before griddepcontrol.wait: CTA i requests slice i of the whole q tensor into L2 (one bulk prefetch).
+// q is an input of the step -- complete before the append that precedes the plan and this kernel in
+// stream order -- and only read here; the Q-quant prologue's loads then hit L2 instead of queueing
+// behind the KV stream's first TMA burst in HBM (CTA-0 timeline: ~5.6K cycles for the amax pass).
+__device__ __forceinline__ void prefetch_q_slice(const DecodeParams& p) {
+  if (threadIdx.x != 0) return;
+  const uint64_t bytes = (uint64_t)p.batch * p.num_heads * 1152u;
+  const uint64_t chunk = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  if (lo >= bytes) return;
+  const uint64_t n = min(chunk, bytes - lo);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p.q) + lo),
+               "r"((uint32_t)n)
+               : "memory");
+}
+
 // x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
 __device__ __forceinline__ float div_by(float x, float s, float rs) {

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   tc_fence_after();
   const uint32_t tmem = lds_u32(BW(tmem_base));
 
+  prefetch_q_slice(p);
   pdl_wait();
   pdl_launch_dependents();
   const int g = blockIdx.x;   // one head tile: a CTA group is one CTA

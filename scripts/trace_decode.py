@@ -66,6 +66,9 @@ print("softmax: S1-SM_in", med(4, 8), "S2-S1", med(8, 9), "S3-S2", med(9, 10), "
 print("corr: C0-prevC_R", np.median((t[13][21:nv] - t[7][20:nv-1])), "C1-C0", med(13, 14), "C_L-C1", med(14, 6), "C2-C_L", med(6, 15), "C_R-C2", med(15, 7))
 
 pro = tr.cpu().numpy()[15 * 256 + 250: 15 * 256 + 255].astype(np.int64)
+qq = tr.cpu().numpy()[15 * 256 + 245: 15 * 256 + 248].astype(np.int64)
+if pro[0] > 0 and qq[0] > 0:
+    print("Q-quant (cycles from kernel entry): start", qq[0] - pro[0], "amax done", qq[1] - pro[0], "codes in TMEM", qq[2] - pro[0])
 if pro[0] > 0:
     print("prologue (cycles from kernel entry): setup done", pro[1] - pro[0], "plan visible", pro[2] - pro[0],
           "Q-quant done", pro[3] - pro[0], "QK sees q_full", pro[4] - pro[0],
