@@ -18,9 +18,10 @@ void mla_debug_set_trace(unsigned long long* dev_buf);
  * kernel (cta_group::2 QK and PV with token / dims halves per CTA of a cluster pair;
  * §7.8), v = 3 the block-pair 2-SM kernel (§7.9).  Process-global. */
 void mla_debug_set_pair(int v);
-/* Kernel for decodes with rows <= 32 (e.g. 16 heads per TP8 rank): v = -1 (default) the
- * swapped-operand kernel (heads on the MMA N dimension), v = 0 the
- * single-CTA kernel (heads padded to M = 64; §7.3).  Process-global. */
+/* Kernel for decodes with rows <= 32 (e.g. 16 heads per TP8 rank): v = 1 the swapped-operand
+ * kernel (heads on the MMA N dimension), v = 0 the single-CTA kernel (heads
+ * padded to M = 64; §7.3), v = -1 (default) the swapped kernel for rows <= 16 and the
+ * single-CTA kernel above.  Process-global. */
 void mla_debug_set_small(int v);
 /* Measurement only (bench.py's roofline denominator): a read-only stream over
  * [buf, buf + bytes) (device memory, 16-B aligned, bytes % 16 == 0), one XOR

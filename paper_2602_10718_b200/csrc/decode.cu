@@ -1549,7 +1549,7 @@ static bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, 
 // (device, pool base, rows, kind).  Nothing else is global.
 std::atomic<unsigned long long*> g_trace{nullptr};
 static std::atomic<int> g_kernel{-1};   // 64 < rows <= 128: -1 auto, 0 single-CTA, 1 block-pair (debug override)
-static std::atomic<int> g_small{-1};    // rows <= 32: -1 auto (swapped-operand kernel), 0 single-CTA (debug override)
+static std::atomic<int> g_small{-1};    // rows <= 32: -1 auto (swapped for <= 16), 1 swapped, 0 single-CTA (debug)
 
 struct DeviceInfo {
   int sms = 0;
@@ -1646,7 +1646,8 @@ using namespace snapmla;
 extern "C" void mla_debug_set_trace(unsigned long long* dev_buf) { g_trace.store(dev_buf); }
 // Debug / test only: force the kernel for 64 < rows <= 128 (-1 = automatic, the default).
 extern "C" void mla_debug_set_pair(int v) { g_kernel.store(v); }
-// Debug / test only: rows <= 32 run the swapped-operand kernel (-1, the default) or the single-CTA one (0).
+// Debug / test only: rows <= 32 run the swapped-operand kernel (1; -1, the default: for rows <= 16, where it
+// is measured faster -- scripts/cmp_small.py) or the single-CTA one (0).
 extern "C" void mla_debug_set_small(int v) { g_small.store(v); }
 extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms) {
   if (batch < 0 || num_heads <= 0) return 0;
@@ -1688,7 +1689,8 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   const int force = g_kernel.load();
   const bool bp = !bf16 && n_ht == 2 &&
                   (force == 1 || (force < 0 && (int64_t)batch * max_pages_per_seq >= kBpMinBlocks));
-  const bool sw = !bf16 && num_heads <= 32 && g_small.load() != 0;
+  const int small = g_small.load();
+  const bool sw = !bf16 && num_heads <= 32 && (small == 1 || (small < 0 && num_heads <= 16));
   int groups = sms / n_ht;
   if (bp) {
     if (!ensure_attr(dev, 2, mla_decode_bp_kernel, kBpSmem)) return MLA_ERR_CUDA;

@@ -11,15 +11,15 @@
 //
 // DESIGN.md §7.11.  Warp roles (16 warps, one CTA per SM, a contiguous range of key blocks from
 // the plan kernel with one head tile):
-//   warps 0-3    softmax (N = 16: a second group, warps 8-11, takes every other block, so two
-//   (8-11)       blocks' reductions are in flight): thread = (token 16 w + lane % 16, heads (lane / 16) N/2 + [0, N/2)):
+//   warps 0-3    softmax (a second group, warps 8-11, takes every other block, so two blocks'
+//   (8-11)       reductions are in flight): thread = (token 16 w + lane % 16, heads (lane / 16) N/2 + [0, N/2)):
 //                Q-quant prologue (Fused-Q-Quant), descale, per-head block max and M_b by
 //                in-warp transpose-butterfly reductions + one SMEM exchange across the 4 warps,
 //                p, w = p sigma_K, P'^T = E4M3(w 448 / M_b) bytes; warp 0 lane h runs head h's
 //                Alg.1 recurrence (m, sigma, l, gamma; state chained in SMEM across the groups in
 //                block order) and the epilogue factors
-//   warps 4-7    accumulators (N = 32: 4-11): O^T <- gamma O^T + T^T per head column; thread =
-//   (4-11)       (dim, N heads) for all 4 dim tiles (N = 32: 2 of them); epilogue o = O f
+//   warps 4-7    accumulators: O^T <- gamma O^T + T^T per head column; thread = (dim, N heads)
+//                for all 4 dim tiles; epilogue o = O f
 //   warp 12      TMA producer (as decode.cu: 4 FP8 boxes + RoPE box + sigma_K per block)
 //   warp 13      QK issuer (A = K tile, B = q codes / q_r' from SMEM)
 //   warp 14      PV issuer (A = V^T MN-major, B = P'^T K-major), 3-slot TMEM ring of T^T
@@ -107,10 +107,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                          const DecodeParams p) {
   using C = SwCfg<N>;
   constexpr int NH = N / 2;
-  // N = 16: two softmax groups (warps 0-3, 8-11) take alternate blocks, 4 accumulator warps (4-7)
-  // hold all 4 dim tiles; N = 32: one softmax group, 8 accumulator warps (4-11) with 2 tiles each
-  constexpr int kGroups = N == 16 ? 2 : 1;
-  constexpr int kAccW = N == 16 ? 4 : 8;
+  // two softmax groups (warps 0-3, 8-11) take alternate blocks, 4 accumulator warps (4-7) hold all
+  // 4 dim tiles (N = 32: 128 O registers each, via setmaxnreg: per SMSP 2 x 144 + 184 + 40 = 512)
+  constexpr int kGroups = 2;
+  constexpr int kAccW = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t bar0 = sbase + C::kOffBar;
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   Unit u;
 
   if (warp >= kSwWarpTma) {
+    if constexpr (N == 32) regs_dec<40>();
     if (warp == kSwWarpTma) {
       // ============================ TMA producer ============================
       if (lane == 0) {
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       }
     }
   } else if (is_sm) {
+    if constexpr (N == 32) regs_inc<144>();
     // ================= softmax: thread = (token, N/2 heads); group grp takes blocks n % kGroups == grp =================
     const int w = warp & 3, hh = lane >> 4, tq = lane & 15;
     const int tok = 16 * w + tq;
@@ -478,6 +480,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     }
   } else {
     // ============ accumulators: thread = (dim, N heads) for kTiles of the 4 dim tiles ============
+    if constexpr (N == 32) regs_inc<184>();
     const int a = warp - kSwWarpAcc, q4 = a & 3, tp = a >> 2;
     constexpr int kTiles = 4 / (kAccW / 4);
     const uint32_t lane_base = (uint32_t)(32 * q4) << 16;
