@@ -91,14 +91,66 @@ static_assert(sizeof(Bars) <= 4096, "barrier region");
 // first_req[g] = request holding block g*per.  Splits fall on 64-token block
 // boundaries, so the result is split-invariant (oracle test
 // test_block_aligned_split_plus_combine_equals_unsplit).
+// Fused-Q-Quant (a2: "per-token scale calculation, mixed-precision conversion and Scale
+// Domain Alignment ... into a single operation"), in the plan launch: CTAs 1.. of the plan grid, one
+// warp per query row (b, h).  Lane l: content dims [16 l, 16 l + 16) -> 16 E4M3 codes (one 16-B
+// store); lanes 0-7 also RoPE dims [8 l, 8 l + 8) -> q_r' = q_r / sigma_q in BF16 (Eq.6).
+// sigma_q = max(amax / 448, 2^-24) (R2), IEEE division; codes = RNE(q / sigma_q) (Markstein).
+__device__ __forceinline__ void q_quant_row(const __nv_bfloat16* __restrict__ q, int row, uint8_t* __restrict__ qc,
+                                            __nv_bfloat16* __restrict__ qr, float* __restrict__ sq) {
+  const int lane = threadIdx.x & 31;
+  const uint4* qrow = reinterpret_cast<const uint4*>(q + (int64_t)row * kDqk);
+  const uint4 v2[2] = {__ldg(qrow + 2 * lane), __ldg(qrow + 2 * lane + 1)};
+  const uint4 vr = lane < 8 ? __ldg(qrow + 64 + lane) : make_uint4(0, 0, 0, 0);
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
+  float amax = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float2 f = __bfloat1622float2(a[e]);
+    amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float s = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
+  const float rs = __frcp_rn(s);
+  uint32_t wd[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
+    const float2 d0 = div_by2(f0, s, rs), d1 = div_by2(f1, s, rs);
+    wd[e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
+  }
+  reinterpret_cast<uint4*>(qc + (int64_t)row * kDc)[lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  if (lane < 8) {
+    const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&vr);
+    uint32_t rw[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(r2[e]);
+      __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, s, rs)), __float2bfloat16_rn(div_by(f.y, s, rs)));
+      rw[e] = *reinterpret_cast<uint32_t*>(&o2);
+    }
+    reinterpret_cast<uint4*>(qr + (int64_t)row * kDr)[lane] = make_uint4(rw[0], rw[1], rw[2], rw[3]);
+  }
+  if (lane == 0) sq[row] = s;
+}
+
 __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ seq_lens, int batch, int num_heads,
                                                     int groups, int32_t* __restrict__ hdr,
                                                     int32_t* __restrict__ cum, int32_t* __restrict__ first_req,
-                                                    int num_sms) {
+                                                    int num_sms, const __nv_bfloat16* __restrict__ q,
+                                                    uint8_t* __restrict__ qc, __nv_bfloat16* __restrict__ qr,
+                                                    float* __restrict__ sq) {
   __shared__ int warp_sums[32];
   __shared__ int s_per;
   const int tid = threadIdx.x;
   pdl_launch_dependents();
+  if (blockIdx.x > 0) {   // Fused-Q-Quant CTAs: 32 rows each (q is an input: no dependence on the append)
+    const int row = (blockIdx.x - 1) * 32 + (tid >> 5);
+    if (row < batch * num_heads) q_quant_row(q, row, qc, qr, sq);
+    pdl_wait();
+    return;
+  }
   const int per_thr = (batch + 1023) / 1024;
   const int b0 = tid * per_thr;
   int local = 0;
@@ -341,7 +393,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_S = tmem;                       // lanes 0-15 (+32k): S slot s at cols 64 s
 
   if (threadIdx.x == 0) TRACE(TR_C2, 251u);   // setup done
-  prefetch_q_slice(p);
   pdl_wait();   // plan (and the appends before it) visible from here on
   pdl_launch_dependents();   // the combine may be scheduled as CTAs retire (it waits for completion)
   if (threadIdx.x == 0) TRACE(TR_C2, 252u);   // plan visible
@@ -454,12 +505,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n = 0, unit = 0;
     while (it.next(u)) {
       // ---------------- Fused-Q-Quant prologue (a2): row r, content half hh
-      if (row_ok) {   // this thread's q lines to L2 up front: the register-limited load rounds below then hit L2
-        const char* qb = reinterpret_cast<const char*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-#pragma unroll
-        for (int l = 0; l < 4; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + 512 * hh + 128 * l));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + 1024 + 64 * hh));
-      }
       if (unit > 0) mbar_wait(BAR(q_free), (unit - 1) & 1, 11, unit);   // QK of the previous unit done
       float c_row;
       if constexpr (kBf) {
@@ -492,67 +537,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(q_full));
       } else {
-        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 245u);   // Q-quant start
-        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-        float amax = 0.f;
-#pragma unroll
-        for (int bh = 0; bh < 4; ++bh) {
-          uint4 qv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + 32 * hh + 8 * bh + i) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(hv[e]);
-              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-            }
-          }
-        }
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
-        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 246u);   // amax done
-        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
-        const float rsq = __frcp_rn(sq);
-        c_row = sq * p.scale_log2;
-        // q_c codes -> TMEM (the QK A operand): this thread's 256 content bytes are TMEM
-        // columns kTmemQ + 64 hh + [0, 64) of its row, 4 codes per column (low byte first)
+        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 245u);   // Q load start
+        // Fused-Q-Quant ran in the plan launch (q_quant_row): load this row's codes (content half hh)
+        // into TMEM columns kTmemQ + 64 hh + [0, 64) (the QK A operand), q_r' into its SW128 SMEM row
+        const int64_t qrow_i = (int64_t)u.b * p.num_heads + head;
+        const uint4* qcr = reinterpret_cast<const uint4*>(p.qc + qrow_i * kDc) + 16 * hh;
+        c_row = (row_ok ? __ldg(p.sq + qrow_i) : 1.f) * p.scale_log2;
 #pragma unroll
         for (int half32 = 0; half32 < 2; ++half32) {
           uint32_t qa[32];
 #pragma unroll
-          for (int g8 = 0; g8 < 8; ++g8) {   // 16-byte chunk of codes (re-read: L1 hit)
-            const int gch = 8 * half32 + g8;
-            uint4 v2[2];
-            v2[0] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch) : make_uint4(0, 0, 0, 0);
-            v2[1] = row_ok ? __ldg(qrow + 32 * hh + 2 * gch + 1) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
-              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
-            }
+          for (int g8 = 0; g8 < 8; ++g8) {
+            const uint4 v = row_ok ? __ldg(qcr + 8 * half32 + g8) : make_uint4(0, 0, 0, 0);
+            qa[4 * g8] = v.x;
+            qa[4 * g8 + 1] = v.y;
+            qa[4 * g8 + 2] = v.z;
+            qa[4 * g8 + 3] = v.w;
           }
           tmem_st_16x32bx2_x32<64>(tmem + lane_off + kTmemQ + 32 * half32, qa);
         }
-        tmem_wait_st();
-        if (threadIdx.x == 32 * kWarpSoftmax && unit == 0) TRACE(TR_C2, 247u);   // codes in TMEM
+        const uint4* qrr = reinterpret_cast<const uint4*>(p.qr + qrow_i * kDr);
 #pragma unroll
         for (int gch = 0; gch < 4; ++gch) {
           const int c = 4 * hh + gch;   // 16-byte chunk of the 128-B RoPE row
-          const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-          uint32_t wd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(a[e]);
-            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
-          }
-          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+          const uint4 v = row_ok ? __ldg(qrr + c) : make_uint4(0, 0, 0, 0);
+          sts_u4(sbase + kOffQr + r * 128 + ((c ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
         }
+        tmem_wait_st();
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
@@ -883,10 +894,8 @@ struct BarsP {
   uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
   uint64_t t_full[2], t_free[2];
   uint64_t q_full, q_free;
-  uint64_t xa_full;                // Q-quant prologue: the 8 accumulator warps' partial amax written
   uint32_t tmem_base;
   float crow[64];
-  float xa[2][64];
   float stat[kPSlots][2][3][64];   // [pair slot][block A / B][m, sigma_p, l][row]
 };
 static_assert(sizeof(BarsP) <= kBpBarBytes, "barrier region (block-pair kernel)");
@@ -971,7 +980,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     }
     mbar_init(BP(q_full), leader ? 12 + 1 : 12);
     mbar_init(BP(q_free), 1);
-    mbar_init(BP(xa_full), 8 * kArriveMul);
     fence_barrier_init();
   }
   if (warp == kBpWarpTma && lane == 0) {
@@ -985,7 +993,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = lds_u32(BP(tmem_base));
 
-  prefetch_q_slice(p);
   pdl_wait();
   pdl_launch_dependents();
   const int ht = (int)cta;
@@ -1194,27 +1201,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
         mbar_wait(BP(q_free), (unit - 1) & 1, 11, unit);
         named_bar_sync(1, 128);
       }
-      mbar_wait(BP(xa_full), unit & 1, 20, unit);   // the accumulator warps' partial amax
-      {
-        const float amax = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
-        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
-        const float rsq = __frcp_rn(sq);
+      {   // Fused-Q-Quant ran in the plan launch: q_r' to its SW128 SMEM row, c = sigma_q scale log2(e)
         if (hk == 0) {
-          const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk);
-          sts_f32(BP(crow) + 4 * r, sq * p.scale_log2);
+          const int64_t qrow_i = (int64_t)u.b * p.num_heads + head;
+          const uint4* qrr = reinterpret_cast<const uint4*>(p.qr + qrow_i * kDr);
+          sts_f32(BP(crow) + 4 * r, (row_ok ? __ldg(p.sq + qrow_i) : 1.f) * p.scale_log2);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const uint4 v = row_ok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-            uint32_t wd[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(a[e]);
-              __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                     __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-              wd[e] = *reinterpret_cast<uint32_t*>(&o2);
-            }
-            sts_u4(sbase + kBpOffQr + r * 128 + ((c ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+            const uint4 v = row_ok ? __ldg(qrr + c) : make_uint4(0, 0, 0, 0);
+            sts_u4(sbase + kBpOffQr + r * 128 + ((c ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
           }
         }
         fence_proxy_async_smem();
@@ -1364,44 +1359,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     while (it.next(u)) {
       if (unit > 0) mbar_wait(BP(q_free), (unit - 1) & 1, 19, unit);
       {
-        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + head) * kDqk) + 32 * cg;
-        float amax = 0.f;
-#pragma unroll 1
-        for (int c8 = 0; c8 < 32; c8 += 8) {
-          uint4 qv[8];
+        // Fused-Q-Quant ran in the plan launch: this thread's 256 codes (dims 256 cg + [0, 256)) into
+        // both TMEM lane halves (the cta_group::2 datapath reads A per N half)
+        const uint4* qcr = reinterpret_cast<const uint4*>(p.qc + ((int64_t)u.b * p.num_heads + head) * kDc) + 16 * cg;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) qv[i] = row_ok ? __ldg(qrow + c8 + i) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(hv[e]);
-              amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-            }
-          }
-        }
-        sts_f32(BP(xa) + 256 * cg + 4 * r, amax);
-        warp_arrive(BP(xa_full), lane);
-        mbar_wait(BP(xa_full), unit & 1, 21, unit);
-        const float am = fmaxf(lds_f32(BP(xa) + 4 * r), lds_f32(BP(xa) + 256 + 4 * r));
-        const float sq = fmaxf(__fdiv_rn(am, 448.0f), kSigmaMin);
-        const float rsq = __frcp_rn(sq);
-#pragma unroll 1
         for (int ci = 0; ci < 2; ++ci) {
           uint32_t qa[32];
 #pragma unroll
           for (int g8 = 0; g8 < 8; ++g8) {
-            uint4 v2[2];
-            v2[0] = row_ok ? __ldg(qrow + 16 * ci + 2 * g8) : make_uint4(0, 0, 0, 0);
-            v2[1] = row_ok ? __ldg(qrow + 16 * ci + 2 * g8 + 1) : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(v2);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-              const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
-              qa[4 * g8 + e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
-            }
+            const uint4 v = row_ok ? __ldg(qcr + 8 * ci + g8) : make_uint4(0, 0, 0, 0);
+            qa[4 * g8] = v.x;
+            qa[4 * g8 + 1] = v.y;
+            qa[4 * g8 + 2] = v.z;
+            qa[4 * g8 + 3] = v.w;
           }
           tmem_st_32x32b_x32(tmem + lane_base + kBpTmemQ + 32 * (2 * cg + ci), qa);
         }
@@ -1612,17 +1582,19 @@ bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap
 }
 
 mla_status launch_plan(const int32_t* seq_lens, int batch, int num_heads, int groups, int32_t* hdr, int32_t* cum,
-                       int32_t* first_req, int num_sms, cudaStream_t st) {
+                       int32_t* first_req, int num_sms, cudaStream_t st, const __nv_bfloat16* q, uint8_t* qc,
+                       __nv_bfloat16* qr, float* sq) {
   cudaLaunchAttribute pdl_attr[1];
   pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t pc = {};
-  pc.gridDim = dim3(1);
+  pc.gridDim = dim3(1 + (q ? (batch * num_heads + 31) / 32 : 0));   // CTA 0 plans, the others quantize q
   pc.blockDim = dim3(1024);
   pc.stream = st;
   pc.attrs = pdl_attr;
   pc.numAttrs = 1;
-  return cudaLaunchKernelEx(&pc, plan_kernel, seq_lens, batch, num_heads, groups, hdr, cum, first_req, num_sms) ==
+  return cudaLaunchKernelEx(&pc, plan_kernel, seq_lens, batch, num_heads, groups, hdr, cum, first_req, num_sms, q, qc,
+                            qr, sq) ==
                  cudaSuccess
              ? MLA_OK
              : MLA_ERR_CUDA;
@@ -1720,7 +1692,12 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   int32_t* cum = reinterpret_cast<int32_t*>(ws + wl.cum);
   int32_t* first = reinterpret_cast<int32_t*>(ws + wl.first);
   cudaStream_t st = (cudaStream_t)stream;
-  if (launch_plan(seq_lens, batch, num_heads, groups, hdr, cum, first, sms, st) != MLA_OK) return MLA_ERR_CUDA;
+  uint8_t* qc = reinterpret_cast<uint8_t*>(ws + wl.qc);
+  __nv_bfloat16* qrp = reinterpret_cast<__nv_bfloat16*>(ws + wl.qr);
+  float* sqp = reinterpret_cast<float*>(ws + wl.sq);
+  if (launch_plan(seq_lens, batch, num_heads, groups, hdr, cum, first, sms, st,
+                  bf16 ? nullptr : static_cast<const __nv_bfloat16*>(q), qc, qrp, sqp) != MLA_OK)
+    return MLA_ERR_CUDA;
 
   const uint32_t smem = bp ? kBpSmem : bf16 ? Variant<true>::kSmem : Variant<false>::kSmem;
   DecodeParams prm;
@@ -1735,6 +1712,9 @@ static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, co
   prm.first_req = first;
   prm.lse_part = reinterpret_cast<float*>(ws + wl.lse);
   prm.o_part = reinterpret_cast<float*>(ws + wl.o);
+  prm.qc = qc;
+  prm.qr = qrp;
+  prm.sq = sqp;
   prm.batch = batch;
   prm.num_heads = num_heads;
   prm.n_ht = n_ht;

@@ -21,6 +21,9 @@ struct DecodeParams {
   const int32_t* first_req;
   float* lse_part;
   float* o_part;
+  const uint8_t* qc;             // Fused-Q-Quant results (written by the plan kernel): E4M3 codes [row][512],
+  const __nv_bfloat16* qr;       //   q_r / sigma_q in BF16 [row][64] (Eq.6), sigma_q [row]; row = b * num_heads + h
+  const float* sq;
   int batch, num_heads, n_ht, max_pages;   // num_heads = rows per request = q_len x heads
   int q_len, heads;                         // MTP: row = t * heads + h for query token t
   float scale_log2;   // softmax_scale * log2(e)
@@ -91,22 +94,6 @@ __device__ __forceinline__ void prefetch_block_table(const int32_t* bt, int k0, 
   for (int j = k0 & ~31; j < k1; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(bt + j));
 }
 
-// Before griddepcontrol.wait: CTA i requests slice i of the whole q tensor into L2 (one bulk prefetch).
-// q is an input of the step -- complete before the append that precedes the plan and this kernel in
-// stream order -- and only read here; the Q-quant prologue's loads then hit L2 instead of queueing
-// behind the KV stream's first TMA burst in HBM (CTA-0 timeline: ~5.6K cycles for the amax pass).
-__device__ __forceinline__ void prefetch_q_slice(const DecodeParams& p) {
-  if (threadIdx.x != 0) return;
-  const uint64_t bytes = (uint64_t)p.batch * p.num_heads * 1152u;
-  const uint64_t chunk = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
-  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
-  if (lo >= bytes) return;
-  const uint64_t n = min(chunk, bytes - lo);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p.q) + lo),
-               "r"((uint32_t)n)
-               : "memory");
-}
-
 // x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
 __device__ __forceinline__ float div_by(float x, float s, float rs) {
@@ -123,7 +110,8 @@ __device__ __forceinline__ float2 div_by2(float2 x, float s, float rs) {
 // Plan (a3) launch shared by the decode entry points: a programmatic dependent of the append,
 // writes hdr / cum / first_req for `groups` CTA groups.
 mla_status launch_plan(const int32_t* seq_lens, int batch, int num_heads, int groups, int32_t* hdr, int32_t* cum,
-                       int32_t* first_req, int num_sms, cudaStream_t st);
+                       int32_t* first_req, int num_sms, cudaStream_t st, const __nv_bfloat16* q = nullptr,
+                       uint8_t* qc = nullptr, __nv_bfloat16* qr = nullptr, float* sq = nullptr);
 // the encoded TMA map of a pool (cached per device; kind 0 FP8 content, 1 BF16 content, 2 RoPE)
 bool cached_tmap(int dev, const void* base, uint64_t rows, int kind, CUtensorMap* out);
 int current_device();

@@ -639,6 +639,9 @@ extern "C" mla_status mla_decode_fp8_mx(const void* q, const uint8_t* kv_fp8, co
   prm.first_req = first;
   prm.lse_part = reinterpret_cast<float*>(ws + wl.lse);
   prm.o_part = reinterpret_cast<float*>(ws + wl.o);
+  prm.qc = nullptr;   // the MX kernel quantizes q in its own prologue
+  prm.qr = nullptr;
+  prm.sq = nullptr;
   prm.batch = batch;
   prm.num_heads = num_heads;
   prm.n_ht = n_ht;

@@ -152,7 +152,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   tc_fence_after();
   const uint32_t tmem = lds_u32(BW(tmem_base));
 
-  prefetch_q_slice(p);
   pdl_wait();
   pdl_launch_dependents();
   const int g = blockIdx.x;   // one head tile: a CTA group is one CTA
@@ -255,54 +254,26 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       // ---------------- Fused-Q-Quant (a2) by group 0: row qr, content chunks of qpart
       if (grp == 0) {
         if (unit > 0) mbar_wait(BW(q_free), (unit - 1) & 1);
+        // Fused-Q-Quant ran in the plan launch: copy row qr's codes (chunks of qpart) into the SW128
+        // B-operand boxes, q_r' into its SW128 row, c = sigma_q scale log2(e)
         const bool rok = qr < p.num_heads;
-        const uint4* qrow = reinterpret_cast<const uint4*>(p.q + ((int64_t)u.b * p.num_heads + qr) * kDqk);
-        constexpr int kCh = 32 / kTpr;               // 16-dim chunks of this thread (2 uint4 each)
-        uint4 qv[2 * kCh];
+        const int64_t qrow_i = (int64_t)u.b * p.num_heads + qr;
+        const uint4* qcr = reinterpret_cast<const uint4*>(p.qc + qrow_i * kDc);
+        const uint4* qrr = reinterpret_cast<const uint4*>(p.qr + qrow_i * kDr);
+        constexpr int kCh = 32 / kTpr;               // 16-code chunks of this thread
 #pragma unroll
-        for (int i = 0; i < 2 * kCh; ++i) qv[i] = rok ? __ldg(qrow + 2 * kCh * qpart + i) : make_uint4(0, 0, 0, 0);
-        float amax = 0.f;
-#pragma unroll
-        for (int i = 0; i < 2 * kCh; ++i) {
-          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&qv[i]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(hv[e]);
-            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-          }
-        }
-#pragma unroll
-        for (int o = 1; o < kTpr; o <<= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        const float sq = fmaxf(__fdiv_rn(amax, 448.0f), kSigmaMin);
-        const float rsq = __frcp_rn(sq);
-#pragma unroll
-        for (int i = 0; i < kCh; ++i) {              // 16 codes -> one 16-B chunk of the SW128 row
+        for (int i = 0; i < kCh; ++i) {
           const int cg = kCh * qpart + i, box = cg >> 3, c16 = cg & 7;
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&qv[2 * i]);
-          uint32_t wd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f0 = __bfloat1622float2(a[2 * e]), f1 = __bfloat1622float2(a[2 * e + 1]);
-            const float2 d0 = div_by2(f0, sq, rsq), d1 = div_by2(f1, sq, rsq);
-            wd[e] = cvt4_e4m3(d0.x, d0.y, d1.x, d1.y);
-          }
-          sts_u4(sbase + C::kOffQc + box * C::kQcBox + qr * 128 + ((c16 ^ (qr & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+          const uint4 v = rok ? __ldg(qcr + cg) : make_uint4(0, 0, 0, 0);
+          sts_u4(sbase + C::kOffQc + box * C::kQcBox + qr * 128 + ((c16 ^ (qr & 7)) << 4), v.x, v.y, v.z, v.w);
         }
 #pragma unroll
-        for (int i = 0; i < 8 / kTpr; ++i) {         // q_r' = q_r / sigma_q (Eq.6), BF16, SW128 row
+        for (int i = 0; i < 8 / kTpr; ++i) {
           const int c = (8 / kTpr) * qpart + i;
-          const uint4 v = rok ? __ldg(qrow + 64 + c) : make_uint4(0, 0, 0, 0);
-          const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-          uint32_t wd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(a[e]);
-            __nv_bfloat162 o2 = __halves2bfloat162(__float2bfloat16_rn(div_by(f.x, sq, rsq)),
-                                                   __float2bfloat16_rn(div_by(f.y, sq, rsq)));
-            wd[e] = *reinterpret_cast<uint32_t*>(&o2);
-          }
-          sts_u4(sbase + C::kOffQr + qr * 128 + ((c ^ (qr & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
+          const uint4 v = rok ? __ldg(qrr + c) : make_uint4(0, 0, 0, 0);
+          sts_u4(sbase + C::kOffQr + qr * 128 + ((c ^ (qr & 7)) << 4), v.x, v.y, v.z, v.w);
         }
+        const float sq = rok ? __ldg(p.sq + qrow_i) : 1.f;
         if (qpart == 0) sts_f32(BW(cq) + 4 * qr, sq * p.scale_log2);
         fence_proxy_async_smem();
         named_bar_sync(nbar, 128);
