@@ -101,7 +101,8 @@ mla_status mla_kv_append_quant(const void* c_kv, const void* k_pe, const int32_t
 /*
  * Workspace bytes that mla_decode_fp8 / mla_combine need for `batch` requests
  * and `num_heads` query heads.  num_sms <= 0 means "the current device".
- * The workspace holds the split plan and the fp32 per-split partials.
+ * The workspace holds the split plan, the Fused-Q-Quant results (E4M3 codes, q_r', sigma_q
+ * per query row) and the fp32 per-split partials.
  */
 size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms);
 
@@ -117,12 +118,15 @@ size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_sms);
  *   w_j = p_j * sigma_K[j], block-wise P quantization P' = E4M3(w * 448 / max_block w),
  *   O <- gamma O + P' V_codes with V = the latent codes, blocks in increasing order.
  * Result (through mla_combine): o = softmax-weighted latent (512), natural-log LSE.
- * Writes only the workspace (split plan + fp32 partials); call mla_combine next.
+ * Writes only the workspace (split plan + quantized q + fp32 partials); call mla_combine next.
+ * Two launches on `stream`: the plan (which also runs Fused-Q-Quant, one warp per q row) and
+ * the decode kernel, a programmatic dependent of it.
  *
  *   q             bf16  [batch, num_heads, 576]
  *   kv_*          the pools written by mla_kv_append_quant (read only)
  *   block_table   int32 [batch, max_pages_per_seq];  seq_lens int32 [batch]
- *   num_heads     1..128 (processed in 64-row head tiles; H < 64 is zero-padded)
+ *   num_heads     1..128 (64-row head tiles, H < 64 zero-padded; H <= 16: heads on the MMA N
+ *                 dimension instead)
  *   softmax_scale multiplies the dequantized logit (e.g. 1/sqrt(192) * mscale^2)
  *   workspace     device buffer of >= mla_decode_workspace_bytes(batch, num_heads, 0)
  */
