@@ -101,6 +101,17 @@ __device__ __forceinline__ float tb_reduce(float (&v)[NH], int lane, int& head) 
   return v[0];
 }
 
+// Wait with a hardware suspend hint: the accumulator and issue warps spend most of the kernel
+// waiting; spinning they take issue slots from the softmax warps on the same SMSPs (the kernel's
+// critical path) -- the thread is woken when the phase completes.
+#ifndef SNAPMLA_SW_SLEEP_NS
+#define SNAPMLA_SW_SLEEP_NS 20000
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
+  while (!mbar_try_wait_ns(a, parity, SNAPMLA_SW_SLEEP_NS)) {
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(kSwThreads, 1)
     mla_decode_sw_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
@@ -191,11 +202,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       // ================================ QK issuer ================================
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        mbar_wait(BW(q_full), unit & 1);
+        mbar_wait_sleep(BW(q_full), unit & 1);
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % C::kSlots, ss = n % kSwSSlots;
-          mbar_wait(BW(kv_full) + 8 * st, (n / C::kSlots) & 1);
-          mbar_wait(BW(s_empty) + 8 * ss, ((n / kSwSSlots) & 1) ^ 1);
+          mbar_wait_sleep(BW(kv_full) + 8 * st, (n / C::kSlots) & 1);
+          mbar_wait_sleep(BW(s_empty) + 8 * ss, ((n / kSwSSlots) & 1) ^ 1);
           tc_fence_after();
           const uint32_t kv = sbase + st * kSwStage, dS = tmem + N * ss;
 #pragma unroll
@@ -220,8 +231,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % C::kSlots, ps = n % kSwPSlots, ts = n % kSwTSlots;
-          mbar_wait(BW(p_full) + 8 * ps, (n / kSwPSlots) & 1);
-          if (n >= (uint32_t)kSwTSlots) mbar_wait(BW(t_free) + 8 * ts, (n / kSwTSlots - 1) & 1);
+          mbar_wait_sleep(BW(p_full) + 8 * ps, (n / kSwPSlots) & 1);
+          if (n >= (uint32_t)kSwTSlots) mbar_wait_sleep(BW(t_free) + 8 * ts, (n / kSwTSlots - 1) & 1);
           tc_fence_after();
           const uint32_t kv = sbase + st * kSwStage, pb = sbase + C::kOffP + ps * C::kPBytes;
           const uint32_t dT = tmem + C::kTmemT + 4 * N * ts;
@@ -464,9 +475,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         for (int h = 0; h < N; ++h) o[d][h] = 0.f;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t ps = n % kSwPSlots, ts = n % kSwTSlots;
-        mbar_wait(BW(p_full) + 8 * ps, (n / kSwPSlots) & 1);
+        mbar_wait_sleep(BW(p_full) + 8 * ps, (n / kSwPSlots) & 1);
         const bool anyskip = lds_f32(BW(skip) + 4 * ps) != 0.f;
-        mbar_wait(BW(t_full) + 8 * ts, (n / kSwTSlots) & 1);
+        mbar_wait_sleep(BW(t_full) + 8 * ts, (n / kSwTSlots) & 1);
         tc_fence_after();
 #pragma unroll
         for (int d = 0; d < kTiles; ++d) {
@@ -497,7 +508,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         warp_arrive(BW(p_empty) + 8 * ps, lane);
       }
       // ---- epilogue (a9): o_part[row h][dim] = O^T[dim][h] f_h
-      mbar_wait(BW(fin_full), unit & 1);
+      mbar_wait_sleep(BW(fin_full), unit & 1);
       const int64_t prow0 = (int64_t)u.slot * kHeadTile;
 #pragma unroll
       for (int d = 0; d < kTiles; ++d) {
