@@ -447,12 +447,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dQr = make_smem_desc(sbase + kOffQr, 16, 1024, LAYOUT_SW128);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        mbar_wait(BAR(q_full), unit & 1, 2, unit);
+        mbar_wait_sleep(BAR(q_full), unit & 1);
         if (lane == 0 && unit == 0) TRACE(TR_C2, 254u);   // QK warp: q_full seen
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % V::kSlots, ss = n % kSSlots;
-          mbar_wait(BAR(kv_full) + 8 * st, (n / V::kSlots) & 1, 3, n);
-          mbar_wait(BAR(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
+          mbar_wait_sleep(BAR(kv_full) + 8 * st, (n / V::kSlots) & 1);
+          mbar_wait_sleep(BAR(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1);
           tc_fence_after();
           if (lane == 0) TRACE(TR_QK, n);
           const uint32_t kv = sbase + V::kOffKv + st * V::kStage;
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % V::kSlots, ps = n % kPSlots;
           const uint32_t h = 2 * n + half, ts = h % V::kTSlots;
-          mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);                  // P'(n) in SMEM
-          if (h >= V::kTSlots) mbar_wait(BAR(t_free) + 8 * ts, (h / V::kTSlots - 1) & 1, 6, n);   // slot read
+          mbar_wait_sleep(BAR(p_full) + 8 * ps, (n / kPSlots) & 1);                  // P'(n) in SMEM
+          if (h >= V::kTSlots) mbar_wait_sleep(BAR(t_free) + 8 * ts, (h / V::kTSlots - 1) & 1);   // slot read
           tc_fence_after();
           if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
           const uint32_t pA = sbase + kOffP + ps * V::kPBytes;
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
       for (int j = u.k0; j < u.k1; ++j, ++n) {
         const uint32_t ps = n % kPSlots;
-        mbar_wait(BAR(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        mbar_wait_sleep(BAR(p_full) + 8 * ps, (n / kPSlots) & 1);
         const uint32_t sa = stat0 + ps * (3 * 64 * 4);
         const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
         warp_arrive(BAR(p_empty) + 8 * ps, lane);                      // stats of this slot consumed
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sig_O = sb;
         }
         const uint32_t h = 2 * n + w, ts = h % V::kTSlots;
-        mbar_wait(BAR(t_full) + 8 * ts, (h / V::kTSlots) & 1, 10, n);      // T half = P'(n) V complete
+        mbar_wait_sleep(BAR(t_full) + 8 * ts, (h / V::kTSlots) & 1);      // T half = P'(n) V complete
         tc_fence_after();
         if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
         const uint32_t taddr = V::t_slot(tmem, ts) + lane_off;

@@ -94,6 +94,21 @@ __device__ __forceinline__ void prefetch_block_table(const int32_t* bt, int k0, 
   for (int j = k0 & ~31; j < k1; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(bt + j));
 }
 
+// Wait with a hardware suspend hint, for warps off the critical path (accumulators and MMA / TMA
+// issuers waiting for work): spinning, they take issue slots -- and power under the board's cap --
+// from the softmax warps on the same SMSPs; the thread is woken when the phase completes.
+#ifndef SNAPMLA_SLEEP_NS
+#define SNAPMLA_SLEEP_NS 20000
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
+#ifdef SNAPMLA_NO_SLEEP
+  mbar_wait(a, parity);
+#else
+  while (!mbar_try_wait_ns(a, parity, SNAPMLA_SLEEP_NS)) {
+  }
+#endif
+}
+
 // x / s for a row-constant s: rcp + one FMA correction of the quotient
 // (Markstein); q codes are not bit-gated (the oracle re-quantizes q itself).
 __device__ __forceinline__ float div_by(float x, float s, float rs) {

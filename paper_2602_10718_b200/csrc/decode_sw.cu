@@ -101,17 +101,6 @@ __device__ __forceinline__ float tb_reduce(float (&v)[NH], int lane, int& head) 
   return v[0];
 }
 
-// Wait with a hardware suspend hint: the accumulator and issue warps spend most of the kernel
-// waiting; spinning they take issue slots from the softmax warps on the same SMSPs (the kernel's
-// critical path) -- the thread is woken when the phase completes.
-#ifndef SNAPMLA_SW_SLEEP_NS
-#define SNAPMLA_SW_SLEEP_NS 20000
-#endif
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
-  while (!mbar_try_wait_ns(a, parity, SNAPMLA_SW_SLEEP_NS)) {
-  }
-}
-
 template <int N>
 __global__ void __launch_bounds__(kSwThreads, 1)
     mla_decode_sw_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,

@@ -73,3 +73,7 @@ if pro[0] > 0:
     print("prologue (cycles from kernel entry): setup done", pro[1] - pro[0], "plan visible", pro[2] - pro[0],
           "Q-quant done", pro[3] - pro[0], "QK sees q_full", pro[4] - pro[0],
           "first TMA", int(t[0][0] - pro[0]), "first QK", int(t[1][0] - pro[0]), "first SM_in", int(t[4][0] - pro[0]))
+
+if nv > 30:
+    sl = slice(20, nv)
+    print("softmax tail: C2-S5 (stats + P' stores)", np.median((t[15] - t[12])[sl]), "SM_out-C2 (fence.proxy.async + arrive)", np.median((t[5] - t[15])[sl]))
