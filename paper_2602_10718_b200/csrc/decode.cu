@@ -883,6 +883,13 @@ constexpr uint32_t kIdescQk16P = make_idesc(1, 1, 0, 0, 128, 128);
 // T half slot h (L = 0, R = 1) at cols 256 + 128 h.
 constexpr uint32_t kBpTmemQ = 128, kBpTmemT = 256;
 
+// The block-pair kernel's MMA issuers and the peer's forwarding warps share SMSPs with the softmax
+// warps; SNAPMLA_BP_SLEEP makes their waits suspend instead of spin (A/B: profiles/r2w_*).
+#ifdef SNAPMLA_BP_SLEEP
+#define SNAPMLA_BP_ISSUE_WAIT(bar, par) mbar_wait_sleep((bar), (par))
+#else
+#define SNAPMLA_BP_ISSUE_WAIT(bar, par) mbar_wait((bar), (par))
+#endif
 struct BarsP {
   alignas(16) uint8_t sink[kPSlots + 1][16];   // landing bytes of the peer's P' / Q signals
   uint64_t kv_full[kBpSlots];    // leader: phase-1 TMA of both CTAs
@@ -1088,12 +1095,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       const uint64_t dQr = make_smem_desc(sbase + kBpOffQr, 16, 1024, LAYOUT_SW128);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        mbar_wait(BP(q_full), unit & 1, 2, unit);
+        SNAPMLA_BP_ISSUE_WAIT(BP(q_full), unit & 1);
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t st = n % kBpSlots, ss = n % kSSlots;
-          mbar_wait(BP(kv_full) + 8 * st, (n / kBpSlots) & 1, 3, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(kv_full) + 8 * st, (n / kBpSlots) & 1);
           if (lane == 0) TRACE(TR_C1, n);
-          mbar_wait(BP(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1, 4, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(s_empty) + 8 * ss, ((n / kSSlots) & 1) ^ 1);
           tc_fence_after();
           if (lane == 0) TRACE(TR_QK, n);
           const uint32_t kv = sbase + kBpOffKv + st * kBpStage;
@@ -1112,17 +1119,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t st = n % kBpSlots, ps = n % kPSlots;
-          mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 5, n);
-          mbar_wait(BP(pp_full) + 8 * ps, (n / kPSlots) & 1, 14, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kPSlots) & 1);
+          SNAPMLA_BP_ISSUE_WAIT(BP(pp_full) + 8 * ps, (n / kPSlots) & 1);
           if (lane == 0 && half == 0) TRACE(TR_S5, n);
-          mbar_wait(BP(v_full) + 8 * st, (n / kBpSlots) & 1, 13, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(v_full) + 8 * st, (n / kBpSlots) & 1);
           if (lane == 0 && half == 0) TRACE(TR_C2, n);
           const uint32_t kv = sbase + kBpOffKv + st * kBpStage;
           const uint32_t pA = sbase + kBpOffP + ps * 8192;
 #pragma unroll
           for (int blk = 0; blk < 2; ++blk) {
             const uint32_t nb = 2 * n + blk;
-            if (nb >= 1) mbar_wait(BP(t_free) + 8 * half, (nb - 1) & 1, 6, n);
+            if (nb >= 1) SNAPMLA_BP_ISSUE_WAIT(BP(t_free) + 8 * half, (nb - 1) & 1);
             tc_fence_after();
             if (lane == 0 && blk == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
             const uint64_t dP = make_smem_desc(pA + 4096 * blk, 1024, 128, LAYOUT_NONE);
@@ -1141,14 +1148,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       const uint32_t q_full_leader = mapa_shared(BP(q_full), 0);
       uint32_t n = 0, unit = 0;
       while (it.next(u)) {
-        mbar_wait(BP(q_full), unit & 1, 18, unit);
+        SNAPMLA_BP_ISSUE_WAIT(BP(q_full), unit & 1);
         tc_fence_after();
         if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(BP(sink), 0) + 16 * kPSlots, sbase + kBpOffQr);
         __syncwarp();
         ++unit;
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t ss = n % kSSlots;
-          mbar_wait(BP(s_empty) + 8 * ss, (n / kSSlots) & 1, 16, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(s_empty) + 8 * ss, (n / kSSlots) & 1);
           if (lane == 0) mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
           __syncwarp();
         }
@@ -1163,7 +1170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
           for (int blk = 0; blk < 2; ++blk, ++nb) {
 #pragma unroll 1
             for (int hf = 0; hf < 2; ++hf) {
-              mbar_wait(BP(t_free) + 8 * hf, nb & 1, 17, nb);
+              SNAPMLA_BP_ISSUE_WAIT(BP(t_free) + 8 * hf, nb & 1);
               if (lane == 0) mbar_arrive_cluster_relaxed(t_free_leader + 8 * hf);
               __syncwarp();
             }
@@ -1177,7 +1184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
           const uint32_t ps = n % kPSlots;
-          mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 15, n);
+          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kPSlots) & 1);
           if (lane == 0)
             mbar_signal_peer_tx(pp_leader + 8 * ps, mapa_shared(BP(sink), 0) + 16 * ps, sbase + kBpOffP + ps * 8192);
           __syncwarp();
