@@ -861,6 +861,10 @@ __device__ __forceinline__ void pv_issue_2sm(uint32_t dT, uint64_t dP, uint64_t 
 // complete on the leader's kv_full / v_full (cta_group::2 TMA), its S-slot and T-half releases
 // and P' readiness are forwarded to the leader by its idle issue warps.
 constexpr int kBpSlots = 4;
+#ifndef SNAPMLA_BP_PSLOTS
+#define SNAPMLA_BP_PSLOTS 2
+#endif
+constexpr int kBpPSlots = SNAPMLA_BP_PSLOTS;   // P' + stats ring depth (block pairs)
 // 16 warps: 0-7 accumulators (2 per SMSP), 8 TMA, 9 QK, 10 / 11 PV_L / PV_R (peer CTA: 9-11
 // forward its signals), 12-15 softmax.  setmaxnreg only redistributes the CTA's launch
 // allocation (512 x 128), so per SMSP 2 x 176 + 40 + 120 = 512 = 4 x 128.  (A 20-warp layout
@@ -872,7 +876,7 @@ static_assert(2 * kBpRegsAcc + kBpRegsSm + kBpRegsIssue <= 4 * 128, "setmaxnreg 
 constexpr uint32_t kBpStage = 41984;   // X 16 KB | Y 16 KB | RoPE 8 KB | sigma_K of A (256 B) and B (256 B)
 constexpr uint32_t kBpOffX = 0, kBpOffY = 16384, kBpOffR = 32768, kBpOffSc = 40960;
 constexpr uint32_t kBpTx1 = 40960, kBpTx2 = 16384;   // TMA bytes per CTA: phase 1 (own block), phase 2 (V half)
-constexpr uint32_t kBpOffQr = 0, kBpOffP = 8192, kBpOffKv = 8192 + kPSlots * 8192;
+constexpr uint32_t kBpOffQr = 0, kBpOffP = 8192, kBpOffKv = 8192 + kBpPSlots * 8192;
 constexpr uint32_t kBpOffBar = kBpOffKv + kBpSlots * kBpStage;
 constexpr uint32_t kBpBarBytes = 8192;
 constexpr uint32_t kBpSmem = kBpOffBar + kBpBarBytes + 1024;
@@ -891,19 +895,19 @@ constexpr uint32_t kBpTmemQ = 128, kBpTmemT = 256;
 #define SNAPMLA_BP_ISSUE_WAIT(bar, par) mbar_wait((bar), (par))
 #endif
 struct BarsP {
-  alignas(16) uint8_t sink[kPSlots + 1][16];   // landing bytes of the peer's P' / Q signals
+  alignas(16) uint8_t sink[kBpPSlots + 1][16];   // landing bytes of the peer's P' / Q signals
   uint64_t kv_full[kBpSlots];    // leader: phase-1 TMA of both CTAs
   uint64_t v_full[kBpSlots];     // leader: phase-2 TMA of both CTAs
   uint64_t sc_full[kBpSlots];    // local: sigma_K of A and B
   uint64_t qk_done[kBpSlots];    // both: QK(pair) complete (multicast commit) -> phase 2 may overwrite
   uint64_t kv_empty[kBpSlots];   // both: PV_L(B) + PV_R(B) complete (multicast commits)
   uint64_t s_full[kSSlots], s_empty[kSSlots];
-  uint64_t p_full[kPSlots], pp_full[kPSlots], p_empty[kPSlots];
+  uint64_t p_full[kBpPSlots], pp_full[kBpPSlots], p_empty[kBpPSlots];
   uint64_t t_full[2], t_free[2];
   uint64_t q_full, q_free;
   uint32_t tmem_base;
   float crow[64];
-  float stat[kPSlots][2][3][64];   // [pair slot][block A / B][m, sigma_p, l][row]
+  float stat[kBpPSlots][2][3][64];   // [pair slot][block A / B][m, sigma_p, l][row]
 };
 static_assert(sizeof(BarsP) <= kBpBarBytes, "barrier region (block-pair kernel)");
 #define BP(field) (bar0 + (uint32_t)offsetof(BarsP, field))
@@ -976,7 +980,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       mbar_init(BP(s_full) + 8 * i, 1);
       mbar_init(BP(s_empty) + 8 * i, leader ? 4 + 1 : 4);
     }
-    for (int i = 0; i < kPSlots; ++i) {
+    for (int i = 0; i < kBpPSlots; ++i) {
       mbar_init(BP(p_full) + 8 * i, 4 * kArriveMul);
       mbar_init(BP(pp_full) + 8 * i, 1);
       mbar_init(BP(p_empty) + 8 * i, 2 + 8 * kArriveMul);
@@ -1118,9 +1122,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       uint32_t n = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
-          const uint32_t st = n % kBpSlots, ps = n % kPSlots;
-          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kPSlots) & 1);
-          SNAPMLA_BP_ISSUE_WAIT(BP(pp_full) + 8 * ps, (n / kPSlots) & 1);
+          const uint32_t st = n % kBpSlots, ps = n % kBpPSlots;
+          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kBpPSlots) & 1);
+          SNAPMLA_BP_ISSUE_WAIT(BP(pp_full) + 8 * ps, (n / kBpPSlots) & 1);
           if (lane == 0 && half == 0) TRACE(TR_S5, n);
           SNAPMLA_BP_ISSUE_WAIT(BP(v_full) + 8 * st, (n / kBpSlots) & 1);
           if (lane == 0 && half == 0) TRACE(TR_C2, n);
@@ -1150,7 +1154,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       while (it.next(u)) {
         SNAPMLA_BP_ISSUE_WAIT(BP(q_full), unit & 1);
         tc_fence_after();
-        if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(BP(sink), 0) + 16 * kPSlots, sbase + kBpOffQr);
+        if (lane == 0) mbar_signal_peer_tx(q_full_leader, mapa_shared(BP(sink), 0) + 16 * kBpPSlots, sbase + kBpOffQr);
         __syncwarp();
         ++unit;
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
@@ -1183,8 +1187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       uint32_t n = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
-          const uint32_t ps = n % kPSlots;
-          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kPSlots) & 1);
+          const uint32_t ps = n % kBpPSlots;
+          SNAPMLA_BP_ISSUE_WAIT(BP(p_full) + 8 * ps, (n / kBpPSlots) & 1);
           if (lane == 0)
             mbar_signal_peer_tx(pp_leader + 8 * ps, mapa_shared(BP(sink), 0) + 16 * ps, sbase + kBpOffP + ps * 8192);
           __syncwarp();
@@ -1228,7 +1232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       const int L = __ldg(p.seq_lens + u.b) - (p.q_len - 1 - head / p.heads);
       float tt[64];
       for (int j = u.k0; j < u.k1; j += 2, ++n) {
-        const uint32_t st = n % kBpSlots, ss = n % kSSlots, ps = n % kPSlots;
+        const uint32_t st = n % kBpSlots, ss = n % kSSlots, ps = n % kBpPSlots;
         const int blk = j + hk;
         const bool valid = blk < u.k1;
         if (j == u.k0) {   // first pair of the unit; later pairs were prefetched (below)
@@ -1334,7 +1338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
           tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss1, *reinterpret_cast<uint32_t(*)[32]>(tt));
           tmem_ld_32x32b_x32(tmem + lane_base + 64 * ss1 + 32, *reinterpret_cast<uint32_t(*)[32]>(tt + 32));
         }
-        mbar_wait(BP(p_empty) + 8 * ps, ((n / kPSlots) & 1) ^ 1, 8, n);
+        mbar_wait(BP(p_empty) + 8 * ps, ((n / kBpPSlots) & 1) ^ 1, 8, n);
         if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_S4, n);
         {
           const uint32_t sa = BP(stat) + ((ps * 2 + hk) * 3 * 64 + r) * 4;
@@ -1393,8 +1397,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
       for (int e = 0; e < 128; ++e) o[e] = 0.f;
       float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
       for (int j = u.k0; j < u.k1; j += 2, ++n) {
-        const uint32_t ps = n % kPSlots;
-        mbar_wait(BP(p_full) + 8 * ps, (n / kPSlots) & 1, 9, n);
+        const uint32_t ps = n % kBpPSlots;
+        mbar_wait(BP(p_full) + 8 * ps, (n / kBpPSlots) & 1, 9, n);
         if (threadIdx.x == 0) TRACE(TR_C0, n);
         const uint32_t sa = BP(stat) + (ps * 2 * 3 * 64 + r) * 4;
         const float mbA = lds_f32(sa), sbA = lds_f32(sa + 256), lbA = lds_f32(sa + 512);
