@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // step 7: sigma_p = max/448, P' = E4M3(w * 448/max); a zero-max block gives
         // P' = 0 and is skipped by the recurrence (R11)
         // BF16 variant: P = BF16(p) with sigma_p = 1 (no P quantization)
-        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = kBf ? 1.f : __fdiv_rn(mb, 448.0f);
+        // sigma_p = M_b / 448 as one multiply by the rounded reciprocal (not bit-gated; as the block-pair kernel)
+        const float st_m = mb > 0.f ? mc : -INFINITY, st_sig = kBf ? 1.f : mb * (1.0f / 448.0f);
         const float inv = mb > 0.f ? __fdividef(448.0f, mb) : 0.f;
         const float2 inv2 = make_float2(inv, inv);
         uint32_t pw[kBf ? 16 : 8];

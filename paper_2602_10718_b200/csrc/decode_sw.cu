@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
               lb += lds_f32(red + 4 * ((2 * 4 + ww) * 32 + h));
             }
             const float mst = mb > 0.f ? (mx_bk == -INFINITY ? 0.f : mx_bk * c_bk) : -INFINITY;   // R11
-            const float sb = __fdiv_rn(mb, 448.0f);
+            const float sb = mb * (1.0f / 448.0f);   // sigma_p = M_b / 448 (one rounding; not bit-gated)
             const bool first = j == u.k0;
             float m_ref = -INFINITY, m_O = 0.f, sig_O = 1.f, l_run = 0.f;
             if (!first) {
