@@ -890,6 +890,14 @@ constexpr uint32_t kBpTmemQ = 128, kBpTmemT = 256;
 
 // The block-pair kernel's MMA issuers and the peer's forwarding warps share SMSPs with the softmax
 // warps; SNAPMLA_BP_SLEEP makes their waits suspend instead of spin (A/B: profiles/r2w_*).
+// SNAPMLA_BP_DIRECT (default 0): the peer CTA's softmax and accumulator warps arrive on the leader's
+// s_empty / t_free themselves (relaxed remote arrives after their TMEM reads completed) instead of
+// arriving locally and having an idle issue warp forward one arrive.  Measured slower on DS-R1
+// (0.503-0.513 vs 0.482 ms decode: 8 remote arrives per T half cost more than the forwarding hop;
+// profiles/r2w_bp_direct_ab_dsr1.txt).
+#ifndef SNAPMLA_BP_DIRECT
+#define SNAPMLA_BP_DIRECT 0
+#endif
 #ifdef SNAPMLA_BP_SLEEP
 #define SNAPMLA_BP_ISSUE_WAIT(bar, par) mbar_wait_sleep((bar), (par))
 #else
@@ -979,7 +987,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(BP(s_full) + 8 * i, 1);
-      mbar_init(BP(s_empty) + 8 * i, leader ? 4 + 1 : 4);
+      mbar_init(BP(s_empty) + 8 * i, leader ? (SNAPMLA_BP_DIRECT ? 4 + 4 : 4 + 1) : 4);
     }
     for (int i = 0; i < kBpPSlots; ++i) {
       mbar_init(BP(p_full) + 8 * i, 4 * kArriveMul);
@@ -988,7 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(BP(t_full) + 8 * i, 1);
-      mbar_init(BP(t_free) + 8 * i, leader ? 8 + 1 : 8);
+      mbar_init(BP(t_free) + 8 * i, leader ? (SNAPMLA_BP_DIRECT ? 8 + 8 : 8 + 1) : 8);
     }
     mbar_init(BP(q_full), leader ? 12 + 1 : 12);
     mbar_init(BP(q_free), 1);
@@ -1159,13 +1167,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
         __syncwarp();
         ++unit;
         for (int j = u.k0; j < u.k1; j += 2, ++n) {
+          if (SNAPMLA_BP_DIRECT) continue;   // the softmax warps arrive on the leader themselves
           const uint32_t ss = n % kSSlots;
           SNAPMLA_BP_ISSUE_WAIT(BP(s_empty) + 8 * ss, (n / kSSlots) & 1);
           if (lane == 0) mbar_arrive_cluster_relaxed(s_empty_leader + 8 * ss);
           __syncwarp();
         }
       }
-    } else if (warp == kBpWarpPv + 1) {
+    } else if (warp == kBpWarpPv + 1 && !SNAPMLA_BP_DIRECT) {
       // ======== peer: forward "T half read" (its 8 accumulator warps) to the leader ========
       const uint32_t t_free_leader = mapa_shared(BP(t_free), 0);
       uint32_t nb = 0;
@@ -1246,7 +1255,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
         if (threadIdx.x == 32 * kBpWarpSm) TRACE(TR_SM_IN, n);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BP(s_empty) + 8 * ss);   // peer: forwarded by its warp 9
+        if (lane == 0) {
+          if (SNAPMLA_BP_DIRECT && !leader) mbar_arrive_cluster_relaxed(mapa_shared(BP(s_empty), 0) + 8 * ss);
+          else mbar_arrive(BP(s_empty) + 8 * ss);   // peer (SNAPMLA_BP_DIRECT 0): forwarded by its warp 9
+        }
         float st_m = -INFINITY, st_sig = 1.f, lsum = 0.f;
         uint32_t pw[16];
         if (valid) {
@@ -1444,7 +1456,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBpThreads, 1)
               else {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(BP(t_free) + 8 * hf);   // peer: forwarded by its warp 11
+                if (lane == 0) {
+                  if (SNAPMLA_BP_DIRECT && !leader) mbar_arrive_cluster_relaxed(mapa_shared(BP(t_free), 0) + 8 * hf);
+                  else mbar_arrive(BP(t_free) + 8 * hf);   // peer (SNAPMLA_BP_DIRECT 0): forwarded by its warp 11
+                }
               }
               const uint32_t* cur = tv[c & 1];
               if (!skip) {
