@@ -1657,9 +1657,11 @@ extern "C" size_t mla_decode_workspace_bytes(int batch, int num_heads, int num_s
 
 // The block-pair kernel wins once each cluster streams enough pairs to amortise its longer
 // start-up; the host cannot read seq_lens (device-resident), so it decides on the block
-// table's extent, an upper bound of the work (scripts/cmp_kernels.py: crossover between
-// 8K and 16K blocks on the DeepSeek-R1 shape).
-constexpr int64_t kBpMinBlocks = 16384;
+// table's extent, an upper bound of the work (scripts/cmp_kernels.py, re-measured after the
+// Q-quant moved into the plan launch: crossover at ~8K blocks on the DeepSeek-R1 shape --
+// 4K blocks tie or favour the single-CTA kernel, 8K+ the block-pair one;
+// profiles/r2x_cmp_kernels_sweep.txt).
+constexpr int64_t kBpMinBlocks = 8192;
 
 static mla_status decode_launch(bool bf16, const void* q, const void* kv_fp8, const void* kv_rope,
                                 const float* kv_scale, const int32_t* block_table, const int32_t* seq_lens,
