@@ -71,6 +71,16 @@ constexpr uint32_t kIdescQk16 = make_idesc(1, 1, 0, 0, 64, 64);     // BF16 x BF
 constexpr uint32_t kIdescPv = make_idesc(0, 0, 0, 1, 64, 256);      // P' K-major, V MN-major
 constexpr uint32_t kIdescQkB = make_idesc(1, 1, 0, 0, 64, 64);      // BF16 variant: q content x K content
 constexpr uint32_t kIdescPvB = make_idesc(1, 1, 0, 1, 64, 256);     // BF16 variant: P K-major, V MN-major
+// FP8 single-CTA kernel, swapped PV (build knob SNAPMLA_SC_SWAPPV, default 0): T^T (dims x 64 heads) =
+// V^T (MN-major) P'^T (K-major), M = 128 dims per tile -- half the M = 64 PV's tensor time.  Correct
+// (the full -m gpu suite passes with it) and it lifts the power-capped clock of the LongCat line from
+// ~1,220 to ~1,510 MHz, but it runs ~14% slower there: every accumulator thread then needs all 64
+// rows' gammas per block (the recurrence moves to warp 11) and T^T has one TMEM slot per half
+// (profiles/r2w_swapped_pv_ab_longcat.txt).
+#ifndef SNAPMLA_SC_SWAPPV
+#define SNAPMLA_SC_SWAPPV 0
+#endif
+constexpr uint32_t kIdescPvSw = make_idesc(0, 0, 1, 0, 128, 64);
 
 struct Bars {
   uint64_t kv_full[5], kv_empty[5];             // TMA -> QK / PV_L + PV_R -> TMA (max over variants)
@@ -78,10 +88,16 @@ struct Bars {
   uint64_t p_full[kPSlots], p_empty[kPSlots];   // P' + stats: softmax -> PV, acc / PV_L + PV_R + acc -> softmax
   uint64_t t_full[3], t_free[3];                // T ring: PV -> WG / WG -> PV
   uint64_t q_full, q_free;                      // Q-quant prologue -> QK / QK of a unit done -> prologue
+  uint64_t fin_full, fin_empty;                 // swapped PV: epilogue factors warp 11 -> accumulators
+  uint64_t gam_full[4], gam_empty[4];           // swapped PV: gamma ring, warp 11 -> accumulators -> warp 11
   uint32_t tmem_base;
   float stat[kPSlots][3][64];         // per block and row: max(t) * c (log2 units), sigma_loc, l_loc
+  alignas(16) float gam[4][64];       // swapped PV: gamma ring (see del)
+  alignas(16) float del[4][64];       // swapped PV: O^T <- gamma O^T + delta T^T per row (head), ring of 4 blocks
+  alignas(16) float skipw[4][4];                  // swapped PV: per block and softmax warp, 1 if some row is skipped (delta = 0)
+  alignas(16) float fin[64];          // swapped PV: epilogue factor per row
 };
-static_assert(sizeof(Bars) <= 4096, "barrier region");
+static_assert(sizeof(Bars) <= 5120, "barrier region");
 #define BAR(field) (bar0 + (uint32_t)offsetof(Bars, field))
 
 // ------------------------------------------------------------------ plan (a3)
@@ -258,13 +274,37 @@ __device__ __forceinline__ void pv_issue(uint32_t dT, uint64_t dP, uint64_t dV, 
       "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z;\n\t"
       "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
+#ifndef SNAPMLA_SOL_NOPV
       "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
       "add.s64 a, %1, 128;\n\tadd.s64 b, %2, 256;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+#endif
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
       ::"r"(dT), "l"(dP), "l"(dV), "r"(kIdescPv), "r"(bar_t), "r"(bar_p), "r"(bar_kv)
+      : "memory");
+}
+
+// One swapped PV half (dim tiles 2 half, 2 half + 1): 2 tiles x 2 K-steps of M = 128, N = 64, K = 32;
+// tile t at TMEM columns dT + 64 t; commit to t_full, p_empty and kv_empty.
+__device__ __forceinline__ void pv_issue_swt(uint32_t dT, uint64_t dV, uint64_t dP, uint32_t bar_t, uint32_t bar_p,
+                                             uint32_t bar_kv) {
+  asm volatile(
+      "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t.reg .b32 z, d;\n\t"
+      "mov.b32 z, 0;\n\tsetp.ne.b32 pf, z, 0;\n\tsetp.eq.b32 pt, z, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 256;\n\tadd.s64 b, %2, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a, b, %3, pt;\n\t"
+      "add.u32 d, %0, 64;\n\tadd.s64 a, %1, 512;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [d], a, %2, %3, pf;\n\t"
+      "add.s64 a, %1, 768;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [d], a, b, %3, pt;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(dT), "l"(dV), "l"(dP), "r"(kIdescPvSw), "r"(bar_t), "r"(bar_p), "r"(bar_kv)
       : "memory");
 }
 
@@ -288,13 +328,13 @@ template <bool kBf> struct Variant;
 template <> struct Variant<false> {
   static constexpr int kSlots = 5, kTSlots = 3, kBoxes = 4;
   static constexpr uint32_t kTx = kKvTx, kStage = 41984, kPBytes = 4096, kOffKv = 16384;
-  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 4096 + 1024;
+  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 5120 + 1024;
   static __device__ __forceinline__ uint32_t t_slot(uint32_t tmem, uint32_t s) { return t_slot_addr(tmem, s); }
 };
 template <> struct Variant<true> {
   static constexpr int kSlots = 2, kTSlots = 2, kBoxes = 8;
   static constexpr uint32_t kTx = 9 * kBoxBytes, kStage = 9 * kBoxBytes, kPBytes = 8192, kOffKv = 8192 + 2 * 8192;
-  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 4096 + 1024;
+  static constexpr uint32_t kOffBar = kOffKv + kSlots * kStage, kSmem = kOffBar + 5120 + 1024;
   static __device__ __forceinline__ uint32_t t_slot(uint32_t tmem, uint32_t s) {
     return tmem + (16u << 16) + 256u * s;
   }
@@ -353,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mla_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_rope,
                       const DecodeParams p) {
   using V = Variant<kBf>;
+  constexpr bool kSwPv = !kBf && SNAPMLA_SC_SWAPPV;   // FP8: PV with swapped operands (T^T, M = 128 dims)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t bar0 = sbase + V::kOffBar;
@@ -367,7 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kPSlots; ++i) {
       mbar_init(BAR(p_full) + 8 * i, 4 * kArriveMul);
-      mbar_init(BAR(p_empty) + 8 * i, 2 + 8 * kArriveMul);   // PV_L + PV_R commits, 8 accumulator warps (stats read)
+      // PV_L + PV_R commits, and the stats readers: the 8 accumulator warps (swapped PV: warp 11)
+      mbar_init(BAR(p_empty) + 8 * i, kSwPv ? 2 + 1 : 2 + 8 * kArriveMul);
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(BAR(s_full) + 8 * i, 1);
@@ -379,6 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(BAR(q_full), 4);
     mbar_init(BAR(q_free), 1);
+    mbar_init(BAR(fin_full), 1);   // swapped PV: warp 11 (the recurrence warp)
+    mbar_init(BAR(fin_empty), 8);  // swapped PV: the 8 accumulator warps
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(BAR(gam_full) + 8 * i, 1);
+      mbar_init(BAR(gam_empty) + 8 * i, 8);
+    }
     fence_barrier_init();
   }
   if (warp == kWarpTma && lane == 0) {
@@ -470,9 +518,80 @@ __global__ void __launch_bounds__(kThreads, 1)
       // =============================== PV_L / PV_R ===============================
       const uint32_t half = warp - kWarpPv;
       uint32_t n = 0;
+      // swapped PV: warp 11 also runs the per-row recurrence (rows lane, lane + 32)
+      float rc_m_ref[2] = {-INFINITY, -INFINITY}, rc_m_O[2] = {0.f, 0.f}, rc_sig_O[2] = {1.f, 1.f}, rc_l[2] = {0.f, 0.f};
+      uint32_t rc_unit = 0;
       while (it.next(u)) {
         for (int j = u.k0; j < u.k1; ++j, ++n) {
           const uint32_t st = n % V::kSlots, ps = n % kPSlots;
+          if constexpr (kSwPv) {   // T^T half `half` (dims 256 half + [0, 256)) -> TMEM cols 256 + 128 half, all lanes
+            mbar_wait_sleep(BAR(p_full) + 8 * ps, (n / kPSlots) & 1);
+            if (half == 1) {
+              // Alg.1 steps 4, 8-10 for rows lane and lane + 32 (as the accumulators of the M = 64 PV
+              // run them per row): gamma / delta into a 4-block ring for the accumulators, whose
+              // threads each need all 64 rows' factors
+              const uint32_t gs = n % 4;
+              if (n >= 4) mbar_wait_sleep(BAR(gam_empty) + 8 * gs, (n / 4 - 1) & 1);
+              bool sk = false;
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int row = lane + 32 * i;
+                const uint32_t sa = BAR(stat) + 4 * row + ps * (3 * 64 * 4);
+                const float mb = lds_f32(sa), sb = lds_f32(sa + 256), lb = lds_f32(sa + 512);
+                const float m_new = fmaxf(rc_m_ref[i], mb);
+                const bool first = j == u.k0;
+                const bool skip = !first && ((mb == -INFINITY) || (mb < m_new - 64.f));
+                float gamma = 0.f, delta = 1.f;
+                if (first) {
+                  rc_m_O[i] = mb;
+                  rc_sig_O[i] = sb;
+                  rc_l[i] = lb;
+                  rc_m_ref[i] = mb;
+                } else if (!skip) {
+                  gamma = ex2_approx(rc_m_O[i] - mb) * __fdividef(rc_sig_O[i], sb);
+                  rc_l[i] = rc_l[i] * ex2_approx(rc_m_ref[i] - m_new) + lb * ex2_approx(mb - m_new);
+                  rc_m_ref[i] = m_new;
+                  rc_m_O[i] = mb;
+                  rc_sig_O[i] = sb;
+                } else {
+                  gamma = 1.f;
+                  delta = 0.f;
+                }
+                sts_f32(BAR(gam) + 4 * (gs * 64 + row), gamma);
+                sts_f32(BAR(del) + 4 * (gs * 64 + row), delta);
+                sk |= skip;
+              }
+              const unsigned any = __ballot_sync(0xffffffffu, sk);
+              if (lane < 4) sts_f32(BAR(skipw) + 4 * (gs * 4 + lane), (lane == 0 && any != 0u) ? 1.f : 0.f);
+              __syncwarp();
+              if (lane == 0) {
+                mbar_arrive(BAR(gam_full) + 8 * gs);
+                mbar_arrive(BAR(p_empty) + 8 * ps);   // stats of this slot consumed
+              }
+              if (j + 1 == u.k1) {   // epilogue factors (a9): o = sigma_O 2^{m_O - m_ref} O / l, natural-log LSE
+                if (rc_unit > 0) mbar_wait_sleep(BAR(fin_empty), (rc_unit - 1) & 1);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                  const int row = lane + 32 * i;
+                  sts_f32(BAR(fin) + 4 * row, rc_l[i] > 0.f ? rc_sig_O[i] * ex2_approx(rc_m_O[i] - rc_m_ref[i]) / rc_l[i] : 0.f);
+                  if (ht * kHeadTile + row < p.num_heads)
+                    p.lse_part[((int64_t)u.slot * p.n_ht + ht) * kHeadTile + row] =
+                        rc_l[i] > 0.f ? (rc_m_ref[i] + log2f(rc_l[i])) * 0.69314718055994531f : -INFINITY;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(BAR(fin_full));
+                ++rc_unit;
+              }
+            }
+            if (n >= 1) mbar_wait_sleep(BAR(t_free) + 8 * half, (n - 1) & 1);
+            tc_fence_after();
+            const uint32_t kvb = sbase + V::kOffKv + st * V::kStage + 2 * half * kBoxBytes;
+            if (lane == 0) TRACE(half == 0 ? TR_PVL : TR_PVR, n);
+            pv_issue_swt(tmem + 256 + 128 * half, make_smem_desc(kvb, kBoxBytes, 1024, LAYOUT_SW128),
+                         make_smem_desc(sbase + kOffP + ps * V::kPBytes, 1024, 128, LAYOUT_NONE),
+                         BAR(t_full) + 8 * half, BAR(p_empty) + 8 * ps, BAR(kv_empty) + 8 * st);
+            continue;
+          }
           const uint32_t h = 2 * n + half, ts = h % V::kTSlots;
           mbar_wait_sleep(BAR(p_full) + 8 * ps, (n / kPSlots) & 1);                  // P'(n) in SMEM
           if (h >= V::kTSlots) mbar_wait_sleep(BAR(t_free) + 8 * ts, (h / V::kTSlots - 1) & 1);   // slot read
@@ -702,6 +821,86 @@ __global__ void __launch_bounds__(kThreads, 1)
         warp_arrive(BAR(p_full) + 8 * ps, lane);
         if (threadIdx.x == 32 * kWarpSoftmax) TRACE(TR_SM_OUT, n);
       }
+      ++unit;
+    }
+  } else if constexpr (kSwPv) {
+    if constexpr (kRegsAcc > 128) regs_inc<kRegsAcc>();
+    else regs_dec<kRegsAcc>();
+    // ==== accumulators (swapped PV): thread = (dim, 64 rows) for dim tiles 2 w, 2 w + 1; O^T in registers ====
+    const int q4 = warp & 3, w = warp >> 2;
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    uint32_t n = 0, unit = 0;
+    while (it.next(u)) {
+      float o[2][64];
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int h = 0; h < 64; ++h) o[d][h] = 0.f;   // the first block enters with gamma = 0
+      for (int j = u.k0; j < u.k1; ++j, ++n) {
+        const uint32_t gs = n % 4;
+        mbar_wait_sleep(BAR(gam_full) + 8 * gs, (n / 4) & 1);            // gamma / delta of block n
+        const float4 sk4 = lds_f4(BAR(skipw) + 16 * gs);
+        const bool anyskip = (sk4.x + sk4.y + sk4.z + sk4.w) != 0.f;
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C0 : TR_C1, n);
+        mbar_wait_sleep(BAR(t_full) + 8 * w, n & 1);                     // T^T half w = V^T P'^T (n) complete
+        tc_fence_after();
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C1 : TR_C2, n);
+        const uint32_t gb = BAR(gam) + 4 * (gs * 64), db = BAR(del) + 4 * (gs * 64);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {   // 16 rows (heads) at a time: their gammas serve both dim tiles
+          float g[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 g4 = lds_f4(gb + 4 * (16 * c + 4 * i));
+            g[4 * i] = g4.x;
+            g[4 * i + 1] = g4.y;
+            g[4 * i + 2] = g4.z;
+            g[4 * i + 3] = g4.w;
+          }
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            uint32_t tv[16];
+            tmem_ld_32x32b_x16(tmem + lane_off + 256 + 128 * w + 64 * d + 16 * c, tv);
+            tmem_wait_ld();
+            if (c == 3 && d == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR(t_free) + 8 * w);            // PV(n + 1) may overwrite the half
+            }
+            if (anyskip) {   // a row whose block is negligible keeps O (delta = 0)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 d4 = lds_f4(db + 4 * (16 * c + 4 * i));
+                tv[4 * i] = __float_as_uint(__uint_as_float(tv[4 * i]) * d4.x);
+                tv[4 * i + 1] = __float_as_uint(__uint_as_float(tv[4 * i + 1]) * d4.y);
+                tv[4 * i + 2] = __float_as_uint(__uint_as_float(tv[4 * i + 2]) * d4.z);
+                tv[4 * i + 3] = __float_as_uint(__uint_as_float(tv[4 * i + 3]) * d4.w);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const int h = 16 * c + e;
+              const float2 r2 = __ffma2_rn(make_float2(o[d][h], o[d][h + 1]), make_float2(g[e], g[e + 1]),
+                                           make_float2(__uint_as_float(tv[e]), __uint_as_float(tv[e + 1])));
+              o[d][h] = r2.x;
+              o[d][h + 1] = r2.y;
+            }
+          }
+        }
+        warp_arrive(BAR(gam_empty) + 8 * gs, lane);                       // this block's factors read
+        if (threadIdx.x == 128 * w) TRACE(w == 0 ? TR_C_L : TR_C_R, n);
+      }
+      // ---------------- epilogue (a9): o_part[row h][dim] = O^T[dim][h] f_h (f from the softmax warps)
+      mbar_wait(BAR(fin_full), unit & 1);
+      const int64_t prow0 = ((int64_t)u.slot * p.n_ht + ht) * kHeadTile;
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const int dim = 128 * (2 * w + d) + 32 * q4 + lane;
+#pragma unroll
+        for (int h = 0; h < 64; ++h)
+          if (ht * kHeadTile + h < p.num_heads) p.o_part[(prow0 + h) * kDc + dim] = o[d][h] * lds_f32(BAR(fin) + 4 * h);
+      }
+      warp_arrive(BAR(fin_empty), lane);
       ++unit;
     }
   } else {

@@ -77,3 +77,7 @@ if pro[0] > 0:
 if nv > 30:
     sl = slice(20, nv)
     print("softmax tail: C2-S5 (stats + P' stores)", np.median((t[15] - t[12])[sl]), "SM_out-C2 (fence.proxy.async + arrive)", np.median((t[5] - t[15])[sl]))
+if nv > 30:
+    sl = slice(20, nv)
+    print("swapped-PV acc (if built): C0->C1 (t_full wait, half L)", np.median((t[14] - t[13])[sl]), "C1->C_L (consume L)", np.median((t[6] - t[14])[sl]),
+          "PVL->C1", np.median((t[14] - t[2])[sl]), "SM_out->PVL", np.median((t[2] - t[5])[sl]))
