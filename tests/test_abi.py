@@ -121,4 +121,9 @@ def test_workspace_size_formula(L):
     # slots = batch + groups; partials = slots * n_ht * 64 rows * 512 fp32
     assert n1 >= (64 + 74) * 2 * 64 * 512 * 4
     assert n2 >= (64 + 148) * 1 * 64 * 512 * 4
+    # plus the plan's Fused-Q-Quant output per query row: 512 E4M3 codes + 64 BF16 q_r' + fp32 sigma_q
+    assert n1 >= (64 + 74) * 2 * 64 * 512 * 4 + 64 * 128 * (512 + 128 + 4)
+    assert n2 >= (64 + 148) * 1 * 64 * 512 * 4 + 64 * 64 * (512 + 128 + 4)
+    grow = L.mla_decode_workspace_bytes(65, 16, 148) - L.mla_decode_workspace_bytes(64, 16, 148)
+    assert grow >= 64 * 512 * 4 + 16 * (512 + 128 + 4) - 3 * 256   # one more slot of partials + 16 rows (alignment slack)
     assert L.mla_decode_workspace_bytes(-1, 16, 148) == 0
