@@ -37,7 +37,7 @@ ct = ct[ct[:, 0] > 0]
 t0g = ct[:, 0].min()
 dur = (ct[:, 1] - ct[:, 0]) / 1e3
 print('CTAs', len(ct), 'start spread us', (ct[:, 0].max() - t0g) / 1e3, 'duration us min/median/max', dur.min(), np.median(dur), dur.max(), 'kernel span us', (ct[:, 1].max() - t0g) / 1e3)
-print('durations sorted (us):', np.round(np.sort(dur)[::10], 1))
+print('durations sorted (us):', np.round(np.sort(dur)[::10], 1)); print('slowest 12 CTAs (us):', ' '.join(f'{x:.1f}' for x in np.sort(dur)[-12:]), '| ids', ' '.join(str(i) for i in np.argsort(dur)[-12:]))
 names = ["TMA", "QK", "PV_L", "PV_R", "SM_in", "SM_out", "C_L", "C_R", "S1", "S2", "S3", "S4", "S5", "C0", "C1", "C2"]
 valid = t[1] > 0
 nv = int(valid.sum())
