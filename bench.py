@@ -81,6 +81,8 @@ def parse():
                     help="NEXT-2: the unquantized BF16 baseline (mla_decode_bf16, same skeleton) on the same workload")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE.json configs[4]: DeepSeek-R1 shape over contexts 4K-128K x batch 1-512")
+    ap.add_argument("--sweep-heads", type=int, default=128,
+                    help="--sweep at another head count per rank (e.g. 16: the TP8 shape's rows)")
     return ap.parse_args()
 
 
@@ -875,14 +877,14 @@ def run_sweep(args, rank, world, local_rank):
             if B * L * BYTES_PER_TOKEN > 60e9:   # keep the pool well inside HBM
                 continue
             a = argparse.Namespace(**vars(args))
-            a.workload, a.batch, a.context, a.heads, a.quick = "dsr1", B, L, 128, True
+            a.workload, a.batch, a.context, a.heads, a.quick = "dsr1", B, L, args.sweep_heads, True
             a.steps, a.warmup = max(5, min(args.steps, 20)), 3
             r = run_ours(a, rank, world, local_rank)
             pts.append({k: r[k] for k in ("batch", "context", "value", "ms_per_step", "decode_ms",
                                           "roofline_frac", "achieved_gbs")} | {"sm_mhz": r["clocks"]["sm_mhz"]})
             torch.cuda.empty_cache()
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "sweep": "BASELINE.json configs[4] (DeepSeek-R1 shape, 128 heads)",
+        print(json.dumps({"metric": METRIC, "sweep": f"BASELINE.json configs[4] (DeepSeek-R1 shape, {args.sweep_heads} heads)",
                           "unit": "tokens/s", "n_gpus": world, "points": pts}))
 
 
