@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(1024) plan_kernel(const int32_t* __restrict__ 
     cum[batch] = total;
     // at least kMinPer blocks per CTA group: a small problem spread one block per group writes (and
     // the combine reads) a 64-row fp32 partial per block -- more bytes than the block's KV itself
-    constexpr int kMinPer = 4;
+#ifndef SNAPMLA_MIN_PER
+#define SNAPMLA_MIN_PER 8
+#endif
+    constexpr int kMinPer = SNAPMLA_MIN_PER;
     const int per = total > 0 ? max((total + groups - 1) / groups, kMinPer) : 1;
     s_per = per;
     hdr[H_TOTAL] = total;
